@@ -1,0 +1,174 @@
+/*
+ * gcnb.h — C ABI of the B200-native row-partitioned GCN training hot path
+ * (arXiv 2212.05009; reference package `gcnpart`, /root/reference/pkg/src/gcnpart).
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t passed
+ * as `void*` (NULL = legacy default stream).  No C++ exceptions cross this
+ * boundary: each function returns a status code and leaves a message readable
+ * through gcnb_last_error() (thread-local).  Status codes mirror the reference's
+ * error classes:
+ *   GCNB_OK      0
+ *   GCNB_EINVAL  1  -> ValueError   (runtime.py:444-445, 482-486; sparse.py:199-200)
+ *   GCNB_ECUDA   2  -> RuntimeError (CUDA launch / memory failure)
+ *   GCNB_ECOMM   3  -> CommError    (runtime.py:47-48, 93-108: missing message / timeout)
+ *   GCNB_EKEY    4  -> KeyError     (sparse.py:249-254: unowned row)
+ *
+ * Storage conventions:
+ *   * dense row blocks are fp32, row-major, row stride `ld` (floats) with
+ *     ld = round_up(d, 4); pad columns are kept at exactly 0.0f;
+ *   * CSR operators are int32 row_ptr (n_rows+1), int32 col, fp32 val; the
+ *     column space of a rank's operator is [own rows | halo rows], the halo
+ *     ordered by sender rank ascending then global id ascending — i.e. the
+ *     concatenation of the reference's per-sender positional blocks
+ *     (runtime.py:203-230, 254-257), so received rows land in place;
+ *   * weights W^k are fp32 [d_{k-1}][ld_k] (column stride padded, pad = 0).
+ *
+ * Deterministic: every reduction (ΔW partials, loss, allreduce) sums in a fixed
+ * order, so reruns are bit-identical (the reference's property, README.md:103-109).
+ */
+#ifndef GCNB_H
+#define GCNB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  GCNB_OK = 0,
+  GCNB_EINVAL = 1,
+  GCNB_ECUDA = 2,
+  GCNB_ECOMM = 3,
+  GCNB_EKEY = 4
+};
+
+enum { GCNB_ACT_RELU = 0, GCNB_ACT_IDENTITY = 1 };
+
+/* ---- library / diagnostics ------------------------------------------- */
+const char* gcnb_last_error(void);
+int gcnb_version(void);
+/* number of kernels this library has launched in this process (all threads) */
+uint64_t gcnb_launch_count(void);
+int gcnb_device_count(int* out);
+
+/* ---- memory (device arenas that can be shared with peer processes) ----- */
+int gcnb_malloc(void** dptr, size_t bytes);
+int gcnb_free(void* dptr);
+int gcnb_memset_async(void* dptr, int value, size_t bytes, void* stream);
+/* cudaIpcMemHandle_t is 64 bytes */
+int gcnb_ipc_get_handle(const void* dptr, uint8_t handle_out[64]);
+int gcnb_ipc_open_handle(const uint8_t handle[64], void** dptr_out);
+int gcnb_ipc_close_handle(void* dptr);
+int gcnb_enable_peer_access(int peer_device);
+
+/* ---- L1 kernels: sparse.py --------------------------------------------- */
+
+/* sparse.spmm (sparse.py:196-207): Y[r] = Σ_j A[r,j]·X[j] for r = rows[i]
+ * (rows == NULL: r = i), i < n_rows.  Row i accumulates its nonzeros in CSR
+ * (ascending column) order; empty rows produce 0. */
+int gcnb_spmm_f32(const int32_t* row_ptr, const int32_t* col, const float* val,
+                  const int32_t* rows, int32_t n_rows,
+                  const float* x, int32_t ldx, int32_t d,
+                  float* y, int32_t ldy, void* stream);
+
+/* sparse.gather_rows (sparse.py:237-261) and the send-side pack of
+ * runtime._fwd_send/_bwd_send (runtime.py:289-294, 336-341), fused with the
+ * point-to-point send of SimNetwork.send (runtime.py:85-91):
+ * segment s (s < n_seg) copies rows x[idx[seg_ptr[s] .. seg_ptr[s+1])] to
+ * dst[s] + i*ld_dst (dst[s] may be a peer-mapped NVLink address).  If
+ * flags != NULL, after all rows of the launch are globally visible the kernel
+ * atomically increments *flags[s] (system scope, release) for every segment
+ * with at least one row — the "message arrived" doorbell used by
+ * gcnb_wait_flags.  `counter` is a device int (zero-initialised once) used for
+ * the last-block election.  Host arrays dst/flags/seg_ptr have n_seg (+1)
+ * entries, n_seg <= GCNB_MAX_PEERS. */
+#define GCNB_MAX_PEERS 64
+int gcnb_pack_rows_f32(const float* x, int32_t ldx, int32_t d,
+                       const int32_t* idx, const int32_t* seg_ptr, int32_t n_seg,
+                       float* const* dst, int32_t ld_dst,
+                       uint64_t* const* flags, int32_t* counter, void* stream);
+
+/* SimNetwork.recv (runtime.py:93-108) for device transports: block the stream
+ * until, for each i < n, flags[srcs[i]] >= ++expected[srcs[i]] (expected is a
+ * device array of per-source counters owned by the receiver).  On timeout
+ * (timeout_ms) the kernel writes 1 to *err and returns; the host maps a
+ * nonzero *err to CommError. */
+int gcnb_wait_flags(const uint64_t* flags, const int32_t* srcs_host, int32_t n,
+                    uint64_t* expected, int32_t* err, int32_t timeout_ms,
+                    void* stream);
+
+/* ---- L6 step functions: runtime.py ------------------------------------- */
+
+/* runtime._fwd_compute (runtime.py:297-306) for the row list `rows`:
+ *   w != NULL:  H[r] = act((A[r,:]·X)·W)      (reference order, X is d_in wide)
+ *   w == NULL:  H[r] = act(A[r,:]·X)          (X already transformed; d_out == d_in)
+ * X is the rank's extended block [own | halo] (row stride ldx), H is written
+ * at the own-row positions (row stride ldh).  act: GCNB_ACT_*. */
+int gcnb_fwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* val,
+                       const int32_t* rows, int32_t n_rows,
+                       const float* x, int32_t ldx, int32_t d_in,
+                       const float* w, int32_t d_out,
+                       float* h, int32_t ldh, int32_t act, void* stream);
+
+/* Dense transform Y = X·W for n_rows contiguous rows (the `@ w` of
+ * runtime.py:299/304 hoisted before aggregation when d_out < d_in). */
+int gcnb_dense_f32(const float* x, int32_t ldx, int32_t n_rows, int32_t d_in,
+                   const float* w, int32_t d_out, float* y, int32_t ldy,
+                   void* stream);
+
+/* runtime._bwd_compute (runtime.py:344-356) for the row list `rows`:
+ *   agg[r]   = A_back[r,:]·G                       (G extended, d_k wide)
+ *   G_prev[r] = (agg[r]·W^T) ⊙ act'(H_prev[r])     if g_prev != NULL (k > 1)
+ *   ΔW_part  += H_prev[r]^T · agg[r]               per block, deterministic
+ * Each launch writes gcnb_bwd_grid(...) partial ΔW blocks of d_prev*ld_k floats
+ * to dw_partials; reduce them with gcnb_reduce_partials_f32.  act'(h) is
+ * (h > 0) for relu (σ'(z) = (z > 0) = (relu(z) > 0), gcn.py:101-104). */
+int gcnb_bwd_grid(int32_t n_rows, int32_t d_prev, int32_t d_k, int32_t with_gprev,
+                  int32_t* grid_out);
+int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* val,
+                       const int32_t* rows, int32_t n_rows,
+                       const float* g, int32_t ldg, int32_t d_k,
+                       const float* h_prev, int32_t ldhp, int32_t d_prev,
+                       const float* w, float* g_prev, int32_t ldgp, int32_t act,
+                       float* dw_partials, void* stream);
+
+/* out[j] = (accumulate ? out[j] : 0) + Σ_{s < n_slots} partials[s*size + j],
+ * summed in slot order (fixed), j < size. */
+int gcnb_reduce_partials_f32(const float* partials, int32_t n_slots, int64_t size,
+                             float* out, int32_t accumulate, void* stream);
+
+/* runtime._local_loss_grad (runtime.py:309-333): for every own row r < n_rows,
+ * label[r] >= 0 marks a labelled row of class label[r].  For labelled rows:
+ * max-shifted log-softmax over the d logits H[r], NLL term, and
+ * G[r] = (softmax - onehot) * inv_n_labeled ⊙ act'(H[r]); unlabelled rows get
+ * G[r] = 0.  *loss_sum (device double) receives Σ NLL over labelled rows,
+ * summed in a fixed order.  `scratch` must hold gcnb_loss_scratch_doubles()
+ * doubles. */
+int gcnb_loss_scratch_doubles(void);
+int gcnb_loss_grad_f32(const float* h, int32_t ldh, int32_t n_rows, int32_t d,
+                       const int32_t* label, double inv_n_labeled,
+                       float* g, int32_t ldg, int32_t act,
+                       double* scratch, double* loss_sum, void* stream);
+
+/* allreduce_sum (runtime.py:147-157): out = bufs[0] + bufs[1] + ... in
+ * ascending rank order (bit-identical on every rank).  bufs is a host array of
+ * p device pointers (local or peer-mapped). */
+int gcnb_sum_buffers_f32(const float* const* bufs, int32_t p, int64_t n,
+                         float* out, void* stream);
+int gcnb_sum_buffers_f64(const double* const* bufs, int32_t p, int64_t n,
+                         double* out, void* stream);
+
+/* runtime._apply_update (runtime.py:359-360): W -= lr·ΔW (n floats). */
+int gcnb_sgd_f32(float* w, const float* dw, int64_t n, float lr, void* stream);
+
+/* fp64 → fp32 with column padding: dst[i*ld_dst + j] = (float)src[i*ld_src + j]
+ * for j < d, 0 for d <= j < ld_dst (host-prepared inputs uploaded as fp64). */
+int gcnb_cast_pad_f64_f32(const double* src, int32_t ld_src, int64_t n_rows,
+                          int32_t d, float* dst, int32_t ld_dst, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GCNB_H */

@@ -1,0 +1,123 @@
+// Library plumbing for the gcnb C ABI: error reporting, launch accounting,
+// device memory that can be mapped into peer processes (CUDA IPC), peer access.
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace gcnb {
+
+std::atomic<uint64_t> g_launches{0};
+
+namespace {
+thread_local char t_err[512] = "";
+int g_sms[MAX_DEVICES] = {0};
+std::mutex g_sms_mu;
+}  // namespace
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return set_error(GCNB_ECUDA, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+int num_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= MAX_DEVICES) return 148;
+  if (g_sms[dev] == 0) {
+    std::lock_guard<std::mutex> lk(g_sms_mu);
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+    g_sms[dev] = n;
+  }
+  return g_sms[dev];
+}
+
+}  // namespace gcnb
+
+using namespace gcnb;
+
+extern "C" const char* gcnb_last_error(void) { return t_err; }
+
+extern "C" int gcnb_version(void) { return 100; }  // 0.1.0
+
+extern "C" uint64_t gcnb_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+extern "C" int gcnb_device_count(int* out) {
+  GCNB_REQUIRE(out != nullptr, "device count: null output");
+  cudaError_t e = cudaGetDeviceCount(out);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_malloc(void** dptr, size_t bytes) {
+  GCNB_REQUIRE(dptr != nullptr, "malloc: null output");
+  cudaError_t e = cudaMalloc(dptr, bytes ? bytes : 16);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_free(void* dptr) {
+  if (!dptr) return GCNB_OK;
+  cudaError_t e = cudaFree(dptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFree");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_memset_async(void* dptr, int value, size_t bytes, void* stream) {
+  if (bytes == 0) return GCNB_OK;
+  GCNB_REQUIRE(dptr != nullptr, "memset: null pointer");
+  cudaError_t e = cudaMemsetAsync(dptr, value, bytes, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_ipc_get_handle(const void* dptr, uint8_t handle_out[64]) {
+  GCNB_REQUIRE(dptr && handle_out, "ipc get handle: null arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dptr));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  std::memcpy(handle_out, &h, 64);
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_ipc_open_handle(const uint8_t handle[64], void** dptr_out) {
+  GCNB_REQUIRE(handle && dptr_out, "ipc open handle: null arguments");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_ipc_close_handle(void* dptr) {
+  if (!dptr) return GCNB_OK;
+  cudaError_t e = cudaIpcCloseMemHandle(dptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_enable_peer_access(int peer_device) {
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return GCNB_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  return GCNB_OK;
+}

@@ -1,0 +1,63 @@
+// Shared helpers for the gcnb sm_100a kernels (error plumbing, launch
+// accounting, small vector math).  See include/gcnb.h for the ABI contract.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+
+#include "../../include/gcnb.h"
+
+namespace gcnb {
+
+constexpr int NT = 256;          // threads per block for the row kernels
+constexpr int WARPS = NT / 32;
+constexpr int RPT_MAX = 8;       // output rows per thread in the tile GEMMs
+constexpr int MAX_DEVICES = 64;
+
+extern std::atomic<uint64_t> g_launches;
+
+int set_error(int code, const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+int num_sms();
+
+// After every <<<>>> launch: surface launch errors, count the launch.
+#define GCNB_AFTER_LAUNCH(what)                                         \
+  do {                                                                  \
+    cudaError_t _e = cudaGetLastError();                                \
+    if (_e != cudaSuccess) return ::gcnb::cuda_fail(_e, what);          \
+    ::gcnb::g_launches.fetch_add(1, std::memory_order_relaxed);         \
+  } while (0)
+
+#define GCNB_REQUIRE(cond, ...)                                         \
+  do {                                                                  \
+    if (!(cond)) return ::gcnb::set_error(GCNB_EINVAL, __VA_ARGS__);    \
+  } while (0)
+
+inline int round4(int d) { return (d + 3) & ~3; }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+__device__ __forceinline__ float4 fma4(float s, const float4& x, float4 a) {
+  a.x = fmaf(s, x.x, a.x);
+  a.y = fmaf(s, x.y, a.y);
+  a.z = fmaf(s, x.z, a.z);
+  a.w = fmaf(s, x.w, a.w);
+  return a;
+}
+
+__device__ __forceinline__ float act_fwd(float z, int act) {
+  return act == GCNB_ACT_RELU ? fmaxf(z, 0.0f) : z;
+}
+
+__device__ __forceinline__ float4 act_fwd4(float4 z, int act) {
+  return make_float4(act_fwd(z.x, act), act_fwd(z.y, act), act_fwd(z.z, act), act_fwd(z.w, act));
+}
+
+// σ'(z) expressed through h = σ(z): relu'(z) = (z > 0) = (h > 0) (gcn.py:101-104).
+__device__ __forceinline__ float act_grad_from_h(float h, int act) {
+  return act == GCNB_ACT_RELU ? (h > 0.0f ? 1.0f : 0.0f) : 1.0f;
+}
+
+}  // namespace gcnb

@@ -1,0 +1,541 @@
+// Row-partitioned GCN layer kernels for sm_100a.
+//
+//   gcnb_spmm_f32       sparse.spmm                (sparse.py:196-207)
+//   gcnb_fwd_layer_f32  runtime._fwd_compute       (runtime.py:297-306)
+//   gcnb_dense_f32      the `@ w` of runtime.py:299 hoisted before aggregation
+//   gcnb_bwd_layer_f32  runtime._bwd_compute       (runtime.py:344-356)
+//
+// Design: the aggregation Σ_j A[r,j]·X[j] is HBM/L2-gather
+// bound.  A group of LPR lanes owns one CSR row; each lane owns a 16-byte
+// float4 chunk of the feature row, so one gather of a neighbour row is a
+// single coalesced LPR×16-byte access.  Column indices and values are loaded
+// cooperatively (one per lane, coalesced) and broadcast with shuffles.  The
+// dense epilogue (·W, ReLU, ·Wᵀ ⊙ σ', Hᵀ·agg) runs on a T-row tile staged in
+// shared memory with W resident in shared memory for the whole persistent
+// block, so the aggregated rows never round-trip through HBM.  All
+// accumulation orders are fixed (CSR order per row, fixed tile→block map,
+// fixed partial-reduction order): reruns are bit-identical.
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace gcnb {
+
+// Cooperative aggregation of one CSR row by a group of LPR lanes.  Must be
+// called by all 32 lanes of the warp (warp-uniform trip count); row < 0
+// marks an idle group.
+template <int LPR, int VPL>
+__device__ __forceinline__ void aggregate_row(const int* __restrict__ rp, const int* __restrict__ col,
+                                              const float* __restrict__ val, int row,
+                                              const float4* __restrict__ X4, int ldx4, int c4, int gl,
+                                              float4 (&acc)[VPL]) {
+  int s = 0, len = 0;
+  if (row >= 0) {
+    s = __ldg(rp + row);
+    len = __ldg(rp + row + 1) - s;
+  }
+  const int maxlen = __reduce_max_sync(0xffffffffu, len);
+  for (int base = 0; base < maxlen; base += LPR) {
+    int cj = 0;
+    float vj = 0.0f;
+    if (base + gl < len) {
+      cj = __ldg(col + s + base + gl);
+      vj = __ldg(val + s + base + gl);
+    }
+    const int cnt = min(LPR, maxlen - base);
+#pragma unroll 8
+    for (int t = 0; t < cnt; ++t) {
+      const int c = __shfl_sync(0xffffffffu, cj, t, LPR);
+      const float v = __shfl_sync(0xffffffffu, vj, t, LPR);
+      if (base + t < len) {
+        const float4* xr = X4 + (size_t)c * ldx4;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const int ch = gl + q * LPR;
+          if (ch < c4) acc[q] = fma4(v, __ldg(xr + ch), acc[q]);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Aggregate-only: Y[r] = act(A[r,:]·X)  (act < 0: plain store)
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const int* __restrict__ col,
+                                            const float* __restrict__ val, const int* __restrict__ rows,
+                                            int n_rows, const float4* __restrict__ X4, int ldx4, int c4,
+                                            float4* __restrict__ Y4, int ldy4, int act) {
+  constexpr int GPW = 32 / LPR;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (LPR - 1);
+  const int gw = lane / LPR;
+  const int warp_global = (blockIdx.x * NT + threadIdx.x) >> 5;
+  const int n_warps = gridDim.x * WARPS;
+  for (int i0 = warp_global * GPW; i0 < n_rows; i0 += n_warps * GPW) {
+    const int i = i0 + gw;
+    int row = -1;
+    if (i < n_rows) row = rows ? __ldg(rows + i) : i;
+    float4 acc[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    aggregate_row<LPR, VPL>(rp, col, val, row, X4, ldx4, c4, gl, acc);
+    if (row >= 0) {
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int ch = gl + q * LPR;
+        if (ch < c4) Y4[(size_t)row * ldy4 + ch] = act >= 0 ? act_fwd4(acc[q], act) : acc[q];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tile GEMM helper: acc[u] (rows trg + u*RG, cols 4tc..4tc+3) += Ys[r][k]·Ws[k][4tc..]
+__device__ __forceinline__ void tile_gemm(const float* __restrict__ Ys, int ys_ld, const float* __restrict__ Ws,
+                                          int ws_ld, int K, int trg, int RG, int tc, int rpt,
+                                          float4 (&acc)[RPT_MAX]) {
+#pragma unroll
+  for (int u = 0; u < RPT_MAX; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4* W4 = reinterpret_cast<const float4*>(Ws);
+  const int ws_ld4 = ws_ld / 4;
+#pragma unroll 4
+  for (int k = 0; k < K; ++k) {
+    const float4 w = W4[k * ws_ld4 + tc];
+#pragma unroll
+    for (int u = 0; u < RPT_MAX; ++u)
+      if (u < rpt) acc[u] = fma4(Ys[(trg + u * RG) * ys_ld + k], w, acc[u]);
+  }
+}
+
+// Stage T rows of the tile into Ys (row stride ys_ld): aggregated (AGG) or
+// loaded directly from X.
+template <int LPR, int VPL, bool AGG>
+__device__ __forceinline__ void stage_tile(const int* __restrict__ rp, const int* __restrict__ col,
+                                           const float* __restrict__ val, const int* __restrict__ rows,
+                                           int n_rows, int t0, int T, const float4* __restrict__ X4, int ldx4,
+                                           int c4, float* __restrict__ Ys, int ys_ld) {
+  if (AGG) {
+    constexpr int NG = NT / LPR;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (LPR - 1);
+    const int grp = threadIdx.x / LPR;
+    for (int r0 = 0; r0 < T; r0 += NG) {
+      const int r = r0 + grp;
+      const int i = t0 + r;
+      int row = -1;
+      if (r < T && i < n_rows) row = rows ? __ldg(rows + i) : i;
+      float4 acc[VPL];
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      aggregate_row<LPR, VPL>(rp, col, val, row, X4, ldx4, c4, gl, acc);
+      if (r < T) {
+        float4* dst = reinterpret_cast<float4*>(Ys + r * ys_ld);
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const int ch = gl + q * LPR;
+          if (ch < c4) dst[ch] = acc[q];
+        }
+      }
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < T * c4; idx += NT) {
+      const int r = idx / c4, ch = idx - r * c4;
+      const int i = t0 + r;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < n_rows) {
+        const int row = rows ? __ldg(rows + i) : i;
+        v = __ldg(X4 + (size_t)row * ldx4 + ch);
+      }
+      reinterpret_cast<float4*>(Ys + r * ys_ld)[ch] = v;
+    }
+  }
+}
+
+// Forward layer with the dense transform fused: H[r] = act((A[r,:]·X)·W)
+// (AGG) or H[r] = act(X[r]·W) (!AGG, the hoisted dense transform).
+template <int LPR, int VPL, bool AGG>
+__global__ void __launch_bounds__(NT) k_fwd_gemm(const int* __restrict__ rp, const int* __restrict__ col,
+                                                 const float* __restrict__ val, const int* __restrict__ rows,
+                                                 int n_rows, const float* __restrict__ X, int ldx, int d_in,
+                                                 const float* __restrict__ W, int d_out, float* __restrict__ H,
+                                                 int ldh, int act, int T) {
+  extern __shared__ __align__(16) float smem[];
+  const int ld_in = (d_in + 3) & ~3;
+  const int ld_out = (d_out + 3) & ~3;
+  const int ys_ld = ld_in + 4;
+  float* Ws = smem;                     // d_in × ld_out
+  float* Ys = smem + d_in * ld_out;     // T × ys_ld
+  {
+    const float4* W4 = reinterpret_cast<const float4*>(W);
+    float4* Ws4 = reinterpret_cast<float4*>(Ws);
+    for (int idx = threadIdx.x; idx < d_in * ld_out / 4; idx += NT) Ws4[idx] = __ldg(W4 + idx);
+  }
+  const int c4o = ld_out / 4;
+  const int RG = NT / c4o;
+  const int tc = threadIdx.x % c4o, trg = threadIdx.x / c4o;
+  const int c4i = ld_in / 4;
+  const int n_tiles = (n_rows + T - 1) / T;
+  const int rpt = trg < RG ? (T - trg + RG - 1) / RG : 0;
+  __syncthreads();
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int t0 = tile * T;
+    stage_tile<LPR, VPL, AGG>(rp, col, val, rows, n_rows, t0, T, reinterpret_cast<const float4*>(X), ldx / 4,
+                              c4i, Ys, ys_ld);
+    __syncthreads();
+    if (rpt > 0) {
+      float4 acc[RPT_MAX];
+      tile_gemm(Ys, ys_ld, Ws, ld_out, d_in, trg, RG, tc, rpt, acc);
+#pragma unroll
+      for (int u = 0; u < RPT_MAX; ++u) {
+        if (u < rpt) {
+          const int i = t0 + trg + u * RG;
+          if (i < n_rows) {
+            const int row = rows ? __ldg(rows + i) : i;
+            reinterpret_cast<float4*>(H + (size_t)row * ldh)[tc] = act_fwd4(acc[u], act);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Backward layer: agg = A_back[r,:]·G;  G_prev[r] = (agg·Wᵀ) ⊙ σ'(H_prev[r]);
+// per-block ΔW partial = Σ_r H_prev[r]ᵀ·agg[r]  (fixed tile order).
+template <int LPR, int VPL, int IPT_MAX>
+__global__ void __launch_bounds__(NT) k_bwd(const int* __restrict__ rp, const int* __restrict__ col,
+                                            const float* __restrict__ val, const int* __restrict__ rows,
+                                            int n_rows, const float* __restrict__ G, int ldg, int d_k,
+                                            const float* __restrict__ Hp, int ldhp, int d_prev,
+                                            const float* __restrict__ W, float* __restrict__ Gp, int ldgp,
+                                            int act, float* __restrict__ partials, int T) {
+  extern __shared__ __align__(16) float smem[];
+  const int ld_k = (d_k + 3) & ~3;
+  const int ld_p = (d_prev + 3) & ~3;
+  const int as_ld = ld_k + 4;
+  const int hs_ld = ld_p + 4;
+  const bool with_gp = Gp != nullptr;
+  float* Wts = smem;                                  // d_k × ld_p  (Wᵀ), only with_gp
+  float* As = smem + (with_gp ? d_k * ld_p : 0);      // T × as_ld
+  float* Hs = As + T * as_ld;                         // T × hs_ld
+  if (with_gp) {
+    for (int idx = threadIdx.x; idx < d_k * ld_p; idx += NT) {
+      const int c = idx / ld_p, i = idx - c * ld_p;
+      Wts[idx] = i < d_prev ? __ldg(W + (size_t)i * ld_k + c) : 0.0f;
+    }
+  }
+  const int c4k = ld_k / 4, c4p = ld_p / 4;
+  // S = agg·Wᵀ mapping (output d_prev wide)
+  const int RG = NT / c4p;
+  const int tc = threadIdx.x % c4p, trg = threadIdx.x / c4p;
+  const int rpt = trg < RG ? (T - trg + RG - 1) / RG : 0;
+  // ΔW mapping: rows i = ig + ii*RGi of ΔW (d_prev), cols 4kc.. (ld_k)
+  const int RGi = NT / c4k;
+  const int kc = threadIdx.x % c4k, ig = threadIdx.x / c4k;
+  const int ipt = ig < RGi && ig < d_prev ? (d_prev - ig + RGi - 1) / RGi : 0;
+  float4 dw[IPT_MAX];
+#pragma unroll
+  for (int ii = 0; ii < IPT_MAX; ++ii) dw[ii] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  const int n_tiles = (n_rows + T - 1) / T;
+  __syncthreads();
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int t0 = tile * T;
+    const int tv = min(T, n_rows - t0);
+    stage_tile<LPR, VPL, true>(rp, col, val, rows, n_rows, t0, T, reinterpret_cast<const float4*>(G), ldg / 4,
+                               c4k, As, as_ld);
+    stage_tile<LPR, VPL, false>(nullptr, nullptr, nullptr, rows, n_rows, t0, T,
+                                reinterpret_cast<const float4*>(Hp), ldhp / 4, c4p, Hs, hs_ld);
+    __syncthreads();
+    if (with_gp && rpt > 0) {
+      float4 acc[RPT_MAX];
+      tile_gemm(As, as_ld, Wts, ld_p, d_k, trg, RG, tc, rpt, acc);
+#pragma unroll
+      for (int u = 0; u < RPT_MAX; ++u) {
+        if (u < rpt) {
+          const int r = trg + u * RG;
+          const int i = t0 + r;
+          if (i < n_rows) {
+            const int row = rows ? __ldg(rows + i) : i;
+            const float4 h = reinterpret_cast<const float4*>(Hs + r * hs_ld)[tc];
+            float4 o = acc[u];
+            o.x *= act_grad_from_h(h.x, act);
+            o.y *= act_grad_from_h(h.y, act);
+            o.z *= act_grad_from_h(h.z, act);
+            o.w *= act_grad_from_h(h.w, act);
+            reinterpret_cast<float4*>(Gp + (size_t)row * ldgp)[tc] = o;
+          }
+        }
+      }
+    }
+    if (ipt > 0) {
+      for (int r = 0; r < tv; ++r) {
+        const float4 a = reinterpret_cast<const float4*>(As + r * as_ld)[kc];
+        const float* hr = Hs + r * hs_ld + ig;
+#pragma unroll
+        for (int ii = 0; ii < IPT_MAX; ++ii)
+          if (ii < ipt) dw[ii] = fma4(hr[ii * RGi], a, dw[ii]);
+      }
+    }
+    __syncthreads();
+  }
+  float* part = partials + (size_t)blockIdx.x * d_prev * ld_k;
+#pragma unroll
+  for (int ii = 0; ii < IPT_MAX; ++ii)
+    if (ii < ipt) reinterpret_cast<float4*>(part + (size_t)(ig + ii * RGi) * ld_k)[kc] = dw[ii];
+  // rows of ΔW no thread owns (d_prev not covered) cannot exist: RGi*IPT >= d_prev by construction.
+}
+
+__global__ void k_reduce_partials(const float* __restrict__ partials, int n_slots, long long size,
+                                  float* __restrict__ out, int accumulate) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < size;
+       j += (long long)gridDim.x * blockDim.x) {
+    float s = accumulate ? out[j] : 0.0f;
+    for (int b = 0; b < n_slots; ++b) s += partials[(size_t)b * size + j];
+    out[j] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+namespace {
+
+struct AggShape {
+  int lpr;
+  int vpl;
+};
+
+AggShape agg_shape(int d) {
+  const int c4 = round4(d) / 4;
+  if (c4 > 32) return {32, (c4 + 31) / 32};
+  int lpr = 1;
+  while (lpr < c4) lpr <<= 1;
+  return {std::max(lpr, 2), 1};
+}
+
+int occupancy_grid(const void* fn, size_t smem, int n_tiles) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, smem) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  return std::max(1, std::min(n_tiles, per_sm * num_sms()));
+}
+
+// Tile height for an output width d_out (RPT_MAX rows per thread at most)
+// that is also a multiple of the aggregation group count NG.
+int tile_rows(int d_out, int lpr) {
+  const int c4o = round4(d_out) / 4;
+  const int rg = NT / c4o;
+  const int ng = NT / lpr;
+  int t = 4 * rg;
+  t = ((t + ng - 1) / ng) * ng;
+  while (t > RPT_MAX * rg && t > ng) t -= ng;
+  return std::max(t, ng);
+}
+
+using AggFn = void (*)(const int*, const int*, const float*, const int*, int, const float4*, int, int, float4*, int,
+                       int);
+AggFn pick_agg(AggShape s) {
+  switch (s.lpr * 4 + s.vpl) {
+    case 2 * 4 + 1: return k_agg<2, 1>;
+    case 4 * 4 + 1: return k_agg<4, 1>;
+    case 8 * 4 + 1: return k_agg<8, 1>;
+    case 16 * 4 + 1: return k_agg<16, 1>;
+    case 32 * 4 + 1: return k_agg<32, 1>;
+    case 32 * 4 + 2: return k_agg<32, 2>;
+    default: return nullptr;
+  }
+}
+
+using FwdFn = void (*)(const int*, const int*, const float*, const int*, int, const float*, int, int, const float*,
+                       int, float*, int, int, int);
+template <bool AGG>
+FwdFn pick_fwd(AggShape s) {
+  switch (s.lpr * 4 + s.vpl) {
+    case 2 * 4 + 1: return k_fwd_gemm<2, 1, AGG>;
+    case 4 * 4 + 1: return k_fwd_gemm<4, 1, AGG>;
+    case 8 * 4 + 1: return k_fwd_gemm<8, 1, AGG>;
+    case 16 * 4 + 1: return k_fwd_gemm<16, 1, AGG>;
+    case 32 * 4 + 1: return k_fwd_gemm<32, 1, AGG>;
+    case 32 * 4 + 2: return k_fwd_gemm<32, 2, AGG>;
+    default: return nullptr;
+  }
+}
+
+using BwdFn = void (*)(const int*, const int*, const float*, const int*, int, const float*, int, int, const float*,
+                       int, int, const float*, float*, int, int, float*, int);
+template <int IPT>
+BwdFn pick_bwd_ipt(AggShape s) {
+  switch (s.lpr * 4 + s.vpl) {
+    case 2 * 4 + 1: return k_bwd<2, 1, IPT>;
+    case 4 * 4 + 1: return k_bwd<4, 1, IPT>;
+    case 8 * 4 + 1: return k_bwd<8, 1, IPT>;
+    case 16 * 4 + 1: return k_bwd<16, 1, IPT>;
+    case 32 * 4 + 1: return k_bwd<32, 1, IPT>;
+    case 32 * 4 + 2: return k_bwd<32, 2, IPT>;
+    default: return nullptr;
+  }
+}
+
+struct BwdPlan {
+  BwdFn fn;
+  int T;
+  size_t smem;
+  int grid;
+};
+
+int bwd_plan(int n_rows, int d_prev, int d_k, bool with_gp, BwdPlan* out) {
+  const AggShape s = agg_shape(d_k);
+  const int ld_k = round4(d_k), ld_p = round4(d_prev);
+  const int c4k = ld_k / 4;
+  const int rgi = NT / c4k;
+  const int ipt = (d_prev + rgi - 1) / rgi;
+  BwdFn fn = nullptr;
+  if (ipt <= 4) fn = pick_bwd_ipt<4>(s);
+  else if (ipt <= 16) fn = pick_bwd_ipt<16>(s);
+  else if (ipt <= 32) fn = pick_bwd_ipt<32>(s);
+  GCNB_REQUIRE(fn != nullptr, "bwd layer: unsupported widths d_prev=%d d_k=%d", d_prev, d_k);
+  const int T = tile_rows(d_prev, s.lpr);
+  const size_t smem =
+      sizeof(float) * ((with_gp ? (size_t)d_k * ld_p : 0) + (size_t)T * (ld_k + 4) + (size_t)T * (ld_p + 4));
+  GCNB_REQUIRE(smem <= 227 * 1024, "bwd layer: tile does not fit shared memory (d_prev=%d d_k=%d)", d_prev, d_k);
+  const int n_tiles = std::max(1, (n_rows + T - 1) / T);
+  out->fn = fn;
+  out->T = T;
+  out->smem = smem;
+  out->grid = occupancy_grid(reinterpret_cast<const void*>(fn), smem, n_tiles);
+  return GCNB_OK;
+}
+
+int check_csr_args(const int32_t* row_ptr, const int32_t* col, const float* val, int32_t n_rows) {
+  GCNB_REQUIRE(n_rows >= 0, "n_rows must be >= 0");
+  GCNB_REQUIRE(n_rows == 0 || (row_ptr && col && val), "CSR arrays must be non-null");
+  return GCNB_OK;
+}
+
+}  // namespace
+}  // namespace gcnb
+
+using namespace gcnb;
+
+extern "C" int gcnb_spmm_f32(const int32_t* row_ptr, const int32_t* col, const float* val, const int32_t* rows,
+                             int32_t n_rows, const float* x, int32_t ldx, int32_t d, float* y, int32_t ldy,
+                             void* stream) {
+  if (int rc = check_csr_args(row_ptr, col, val, n_rows)) return rc;
+  GCNB_REQUIRE(d >= 1 && d <= 256, "spmm: width d=%d out of range [1, 256]", d);
+  GCNB_REQUIRE(ldx % 4 == 0 && ldy % 4 == 0 && ldx >= round4(d) && ldy >= round4(d),
+               "spmm: row strides must be multiples of 4 and >= round4(d)");
+  GCNB_REQUIRE(aligned16(x) && aligned16(y), "spmm: X and Y must be 16-byte aligned");
+  if (n_rows == 0) return GCNB_OK;
+  const AggShape s = agg_shape(d);
+  AggFn fn = pick_agg(s);
+  const int rows_per_block = NT / s.lpr;
+  const int grid = std::max(1, std::min((n_rows + rows_per_block - 1) / rows_per_block, num_sms() * 8));
+  fn<<<grid, NT, 0, (cudaStream_t)stream>>>(row_ptr, col, val, rows, n_rows, reinterpret_cast<const float4*>(x),
+                                            ldx / 4, round4(d) / 4, reinterpret_cast<float4*>(y), ldy / 4, -1);
+  GCNB_AFTER_LAUNCH("spmm");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_fwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* val,
+                                  const int32_t* rows, int32_t n_rows, const float* x, int32_t ldx, int32_t d_in,
+                                  const float* w, int32_t d_out, float* h, int32_t ldh, int32_t act,
+                                  void* stream) {
+  if (int rc = check_csr_args(row_ptr, col, val, n_rows)) return rc;
+  GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "fwd layer: unknown activation %d", act);
+  GCNB_REQUIRE(d_in >= 1 && d_in <= 256 && d_out >= 1 && d_out <= 256, "fwd layer: widths out of range");
+  GCNB_REQUIRE(w != nullptr || d_out == d_in, "fwd layer: without W, d_out must equal d_in");
+  GCNB_REQUIRE(ldx % 4 == 0 && ldh % 4 == 0 && ldx >= round4(d_in) && ldh >= round4(d_out),
+               "fwd layer: row strides must be multiples of 4 and cover the widths");
+  GCNB_REQUIRE(aligned16(x) && aligned16(h) && (!w || aligned16(w)), "fwd layer: operands must be 16-byte aligned");
+  if (n_rows == 0) return GCNB_OK;
+  const AggShape s = agg_shape(d_in);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!w) {
+    AggFn fn = pick_agg(s);
+    const int rows_per_block = NT / s.lpr;
+    const int grid = std::max(1, std::min((n_rows + rows_per_block - 1) / rows_per_block, num_sms() * 8));
+    fn<<<grid, NT, 0, st>>>(row_ptr, col, val, rows, n_rows, reinterpret_cast<const float4*>(x), ldx / 4,
+                            round4(d_in) / 4, reinterpret_cast<float4*>(h), ldh / 4, act);
+    GCNB_AFTER_LAUNCH("fwd layer (aggregate)");
+    return GCNB_OK;
+  }
+  FwdFn fn = pick_fwd<true>(s);
+  const int T = tile_rows(d_out, s.lpr);
+  const size_t smem = sizeof(float) * ((size_t)d_in * round4(d_out) + (size_t)T * (round4(d_in) + 4));
+  GCNB_REQUIRE(smem <= 227 * 1024, "fwd layer: tile does not fit shared memory");
+  const int grid = occupancy_grid(reinterpret_cast<const void*>(fn), smem, (n_rows + T - 1) / T);
+  fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, x, ldx, d_in, w, d_out, h, ldh, act, T);
+  GCNB_AFTER_LAUNCH("fwd layer (aggregate+transform)");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_dense_f32(const float* x, int32_t ldx, int32_t n_rows, int32_t d_in, const float* w,
+                              int32_t d_out, float* y, int32_t ldy, void* stream) {
+  GCNB_REQUIRE(n_rows >= 0, "dense: n_rows must be >= 0");
+  GCNB_REQUIRE(d_in >= 1 && d_in <= 256 && d_out >= 1 && d_out <= 256, "dense: widths out of range");
+  GCNB_REQUIRE(ldx % 4 == 0 && ldy % 4 == 0 && ldx >= round4(d_in) && ldy >= round4(d_out),
+               "dense: row strides must be multiples of 4 and cover the widths");
+  GCNB_REQUIRE(x && w && y && aligned16(x) && aligned16(w) && aligned16(y), "dense: operands must be 16-byte aligned");
+  if (n_rows == 0) return GCNB_OK;
+  const AggShape s = agg_shape(d_in);
+  FwdFn fn = pick_fwd<false>(s);
+  const int T = tile_rows(d_out, s.lpr);
+  const size_t smem = sizeof(float) * ((size_t)d_in * round4(d_out) + (size_t)T * (round4(d_in) + 4));
+  GCNB_REQUIRE(smem <= 227 * 1024, "dense: tile does not fit shared memory");
+  const int grid = occupancy_grid(reinterpret_cast<const void*>(fn), smem, (n_rows + T - 1) / T);
+  fn<<<grid, NT, smem, (cudaStream_t)stream>>>(nullptr, nullptr, nullptr, nullptr, n_rows, x, ldx, d_in, w, d_out,
+                                               y, ldy, GCNB_ACT_IDENTITY, T);
+  GCNB_AFTER_LAUNCH("dense");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_bwd_grid(int32_t n_rows, int32_t d_prev, int32_t d_k, int32_t with_gprev, int32_t* grid_out) {
+  GCNB_REQUIRE(grid_out != nullptr, "bwd grid: null output");
+  GCNB_REQUIRE(d_prev >= 1 && d_prev <= 256 && d_k >= 1 && d_k <= 256, "bwd grid: widths out of range");
+  BwdPlan plan;
+  if (int rc = bwd_plan(n_rows, d_prev, d_k, with_gprev != 0, &plan)) return rc;
+  *grid_out = plan.grid;
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* val,
+                                  const int32_t* rows, int32_t n_rows, const float* g, int32_t ldg, int32_t d_k,
+                                  const float* h_prev, int32_t ldhp, int32_t d_prev, const float* w,
+                                  float* g_prev, int32_t ldgp, int32_t act, float* dw_partials, void* stream) {
+  if (int rc = check_csr_args(row_ptr, col, val, n_rows)) return rc;
+  GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "bwd layer: unknown activation %d", act);
+  GCNB_REQUIRE(d_prev >= 1 && d_prev <= 256 && d_k >= 1 && d_k <= 256, "bwd layer: widths out of range");
+  GCNB_REQUIRE(ldg % 4 == 0 && ldhp % 4 == 0 && ldg >= round4(d_k) && ldhp >= round4(d_prev),
+               "bwd layer: row strides must be multiples of 4 and cover the widths");
+  GCNB_REQUIRE(!g_prev || (ldgp % 4 == 0 && ldgp >= round4(d_prev) && aligned16(g_prev) && w && aligned16(w)),
+               "bwd layer: G_prev needs W and an aligned stride >= round4(d_prev)");
+  GCNB_REQUIRE(g && h_prev && dw_partials && aligned16(g) && aligned16(h_prev) && aligned16(dw_partials),
+               "bwd layer: operands must be non-null and 16-byte aligned");
+  BwdPlan plan;
+  if (int rc = bwd_plan(n_rows, d_prev, d_k, g_prev != nullptr, &plan)) return rc;
+  plan.fn<<<plan.grid, NT, plan.smem, (cudaStream_t)stream>>>(row_ptr, col, val, rows, n_rows, g, ldg, d_k, h_prev,
+                                                              ldhp, d_prev, w, g_prev, ldgp, act, dw_partials,
+                                                              plan.T);
+  GCNB_AFTER_LAUNCH("bwd layer");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_reduce_partials_f32(const float* partials, int32_t n_slots, int64_t size, float* out,
+                                        int32_t accumulate, void* stream) {
+  GCNB_REQUIRE(n_slots >= 0 && size >= 0, "reduce partials: negative sizes");
+  GCNB_REQUIRE(out && (n_slots == 0 || partials), "reduce partials: null operands");
+  if (size == 0) return GCNB_OK;
+  const int grid = (int)std::min<int64_t>((size + NT - 1) / NT, num_sms() * 4);
+  k_reduce_partials<<<grid, NT, 0, (cudaStream_t)stream>>>(partials, n_slots, size, out, accumulate);
+  GCNB_AFTER_LAUNCH("reduce partials");
+  return GCNB_OK;
+}

@@ -1,0 +1,661 @@
+"""Device runtime of the row-partitioned GCN training path (mirrors gcnpart.runtime).
+
+Public surface (runtime.py:44-632 of the reference):
+`scatter`, `train_epochs`, `parallel_feedforward`, `parallel_backprop`,
+`ProcState`, `EpochMetrics`, `MessageRecord`, `CommError`, `FullBatch`,
+`MiniBatch`, `allreduce_sum`, and `DeviceNetwork` (the SimNetwork stand-in).
+
+All ranks of a single process live on one CUDA device and run in the
+reference's "round" order on one stream: for each layer every rank packs its
+boundary rows straight into the receivers' halo slots, then every rank runs
+its fused layer kernel.  Stream order is the message ordering, so there is
+no flag traffic inside one process.  One-process-per-GPU training (the
+scaling path, NVLink peer stores + doorbells) is `distributed.py`; both use
+the same per-rank step methods defined here.
+
+Numerics: fp32 with fixed accumulation order (deterministic reruns).  The
+ΔW of every layer is reduced per rank, summed over ranks in ascending rank
+order (allreduce_sum, runtime.py:147-157), and applied with plain SGD at the
+end of the backward sweep.  Deferring the updates is exact: layer k's
+backward uses W^k before its update (runtime.py:353 runs before 386-387) and
+no layer < k reads W^k.
+"""
+
+from __future__ import annotations
+
+import queue
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, devmem
+from ._lib import CommError
+from .comm import CommPlan, build_comm_plan
+from .host import GcnModel, LabelSet, MiniBatchSpec, induced_pattern
+from .layout import OpLayout, RankLayout, build_rank_layout
+from .sparse import dense, normalize_adjacency, transpose_sparse
+
+SCHEDULERS = ("round", "threads")
+
+
+@dataclass(frozen=True)
+class MessageRecord:
+    """One point-to-point message (runtime.py:51-64).  `cols` is the
+    reference-equivalent row width (d_{k-1} forward, d_k backward); `nbytes`
+    is what the device actually moved."""
+
+    epoch: int
+    step: int
+    phase: str
+    layer: int
+    src: int
+    dst: int
+    rows: int
+    cols: int
+    nbytes: int = 0
+
+    @property
+    def words(self) -> int:
+        return self.rows * self.cols
+
+
+@dataclass(frozen=True)
+class EpochMetrics:
+    total_words: int
+    max_words_per_proc: int
+    avg_words_per_proc: float
+    total_msgs: int
+    max_msgs_per_proc: int
+    wallclock: float
+    loss: float
+
+
+@dataclass(frozen=True)
+class FullBatch:
+    pass
+
+
+@dataclass(frozen=True)
+class MiniBatch:
+    """Per-step uniform vertex sampling under the fixed partition (runtime.py:543-554)."""
+
+    spec: MiniBatchSpec
+    batches_per_epoch: int
+    seed: int
+    adjacency: object
+    features: np.ndarray
+    owner: np.ndarray
+    directed: bool = False
+
+
+class DeviceNetwork:
+    """SimNetwork-compatible accounting front of the device transport (runtime.py:67-144).
+
+    The device path never routes payloads through this object: it records
+    the plan-derived MessageRecord of every transfer the kernels perform.
+    `send`/`recv` keep the reference's host FIFO semantics (tag and shape
+    checks, CommError) for callers that exchange host arrays directly.
+    """
+
+    def __init__(self, p: int):
+        self.p = p
+        self.log: list = []
+        self._lock = threading.Lock()
+        self._queues = {(s, d): queue.Queue() for s in range(p) for d in range(p) if s != d}
+
+    def send(self, src: int, dst: int, payload, tag) -> None:
+        if src == dst:
+            raise CommError("a rank never messages itself")
+        payload = np.asarray(payload)
+        self._log(MessageRecord(*tag, src=src, dst=dst, rows=payload.shape[0], cols=payload.shape[1]))
+        self._queues[(src, dst)].put((tag, payload))
+
+    def recv(self, dst: int, src: int, tag, expect_shape):
+        try:
+            got_tag, payload = self._queues[(src, dst)].get(block=False)
+        except queue.Empty:
+            raise CommError(f"rank {dst} expected a message from rank {src} at {tag} but none arrived") from None
+        if got_tag != tag:
+            raise CommError(f"rank {dst} got message tagged {got_tag}, expected {tag}")
+        if tuple(payload.shape) != tuple(expect_shape):
+            raise CommError(f"payload from {src} to {dst} has shape {payload.shape}, expected {expect_shape}")
+        return payload
+
+    def _log(self, rec: MessageRecord) -> None:
+        with self._lock:
+            self.log.append(rec)
+
+    def records(self, epoch: int | None = None, step: int | None = None) -> list:
+        with self._lock:
+            recs = list(self.log)
+        if epoch is not None:
+            recs = [r for r in recs if r.epoch == epoch]
+        if step is not None:
+            recs = [r for r in recs if r.step == step]
+        return recs
+
+
+SimNetwork = DeviceNetwork
+
+
+def _net_log(net, rec: MessageRecord) -> None:
+    if hasattr(net, "_log"):
+        net._log(rec)
+    else:  # a gcnpart.SimNetwork: append to its log list
+        net.log.append(rec)
+
+
+def _net_records(net, epoch=None, step=None) -> list:
+    return net.records(epoch=epoch, step=step)
+
+
+def allreduce_sum(contributions) -> np.ndarray:
+    """Host elementwise sum in ascending rank order (runtime.py:147-157)."""
+    mats = [dense(c) for c in contributions]
+    for c in mats[1:]:
+        if c.shape != mats[0].shape:
+            raise ValueError(f"allreduce shape mismatch: {c.shape} vs {mats[0].shape}")
+    out = mats[0].copy()
+    for c in mats[1:]:
+        out += c
+    return out
+
+
+# ---------------------------------------------------------------------------
+# per-rank device state
+
+
+class _DeviceOp:
+    """Device copy of one OpLayout."""
+
+    def __init__(self, lay: OpLayout, dev):
+        self.lay = lay
+        self.csr = devmem.upload_csr_arrays(lay.n_own, lay.n_cols, lay.row_ptr, lay.col, lay.val, dev)
+        self.interior = devmem.upload_index(lay.interior, dev)
+        self.boundary = devmem.upload_index(lay.boundary, dev)
+        self.send_idx = devmem.upload_index(lay.send_idx, dev)
+
+
+class _WeightList(list):
+    """Host view of a rank's weights; item assignment uploads (runtime.py:181 semantics)."""
+
+    def __init__(self, st: "ProcState", items):
+        super().__init__(items)
+        self._st = st
+
+    def __setitem__(self, k, value):
+        super().__setitem__(k, value)
+        self._st._upload_weight(k, value)
+
+
+class ProcState:
+    """Everything one rank stores, resident on its CUDA device (runtime.py:160-189).
+
+    Reference-visible attributes (`rank`, `global_rows`, `plan_fwd`,
+    `plan_bwd`, `dims`, `activation`, `learning_rate`, `h0`, `h`, `g`,
+    `weights`, `a_fwd_local`, `a_fwd_recv`, ...) are host views: scalars and
+    plans are kept on the host, activations and weights are downloaded on
+    access.  `weights` supports item assignment (uploads that replica only).
+    """
+
+    def __init__(self, layout: RankLayout, plan_fwd: CommPlan, plan_bwd: CommPlan, model, h0: np.ndarray, dev):
+        self.rank = layout.rank
+        self.global_rows = layout.global_rows
+        self.plan_fwd = plan_fwd
+        self.plan_bwd = plan_bwd
+        self.dims = tuple(int(d) for d in model.dims)
+        self.activation = model.activation
+        self.learning_rate = float(model.learning_rate)
+        self.layout = layout
+        self.device = dev
+        self._h0_host = np.ascontiguousarray(h0)
+        self._has_trace = False
+        self._has_grad = False
+        L = self.n_layers
+        n = len(layout.global_rows)
+        self.n_own = n
+        self.act = _lib.ACT[self.activation]
+        with torch.cuda.device(dev):
+            self.op_fwd = _DeviceOp(layout.fwd, dev)
+            self.op_bwd = self.op_fwd if layout.bwd is layout.fwd else _DeviceOp(layout.bwd, dev)
+            # layer k transforms first (H·W then aggregate) when that narrows the halo/gather
+            self.transform_first = [False] + [self.dims[k] < self.dims[k - 1] for k in range(1, L + 1)]
+            R_f, R_b = layout.fwd.n_halo, layout.bwd.n_halo
+            self.xext = [None] * (L + 1)   # operand of forward layer k: [own | halo]
+            self.hbuf = [None] * (L + 1)   # H^k own rows
+            for k in range(1, L + 1):
+                width = self.dims[k] if self.transform_first[k] else self.dims[k - 1]
+                self.xext[k] = devmem.empty_rows(n + R_f, width, dev)
+            for k in range(0, L + 1):
+                if k < L and not self.transform_first[k + 1]:
+                    self.hbuf[k] = self.xext[k + 1][:n]
+                else:
+                    self.hbuf[k] = devmem.empty_rows(n, self.dims[k], dev)
+            self.hbuf[0][:, : self.dims[0]].copy_(torch.from_numpy(np.asarray(h0, dtype=np.float32)))
+            self.gext = [None] + [devmem.empty_rows(n + R_b, self.dims[k], dev) for k in range(1, L + 1)]
+            self.w = [None] + [devmem.empty_rows(self.dims[k - 1], self.dims[k], dev) for k in range(1, L + 1)]
+            for k in range(1, L + 1):
+                self._upload_weight(k - 1, model.weights[k - 1])
+            self.dw = [None] + [torch.zeros_like(self.w[k]) for k in range(1, L + 1)]
+            self.dw_sum = [None] + [torch.zeros_like(self.w[k]) for k in range(1, L + 1)]
+            self.dw_total = [None] * (L + 1)  # allreduced ΔW of the last backward sweep
+            # ΔW partial slots: interior launch + boundary launch (or one all-rows launch)
+            self.bwd_grids = [None] * (L + 1)
+            self.partials = [None] * (L + 1)
+            for k in range(1, L + 1):
+                with_gp = k > 1
+                gi = _lib.bwd_grid(len(layout.bwd.interior), self.dims[k - 1], self.dims[k], with_gp)
+                gb = _lib.bwd_grid(len(layout.bwd.boundary), self.dims[k - 1], self.dims[k], with_gp)
+                ga = _lib.bwd_grid(n, self.dims[k - 1], self.dims[k], with_gp)
+                self.bwd_grids[k] = (gi, gb, ga)
+                slots = max(gi + gb, ga)
+                self.partials[k] = torch.zeros((slots, self.dims[k - 1] * devmem.ld_of(self.dims[k])),
+                                               dtype=torch.float32, device=dev)
+            self.label = torch.full((max(n, 1),), -1, dtype=torch.int32, device=dev)
+            self.loss_scratch = torch.zeros(_lib.loss_scratch_doubles(), dtype=torch.float64, device=dev)
+            self.loss_sum = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    # -- reference-compatible host views ---------------------------------
+    @property
+    def n_layers(self) -> int:
+        return len(self.dims) - 1
+
+    @property
+    def h0(self) -> np.ndarray:
+        return self._h0_host
+
+    @property
+    def h(self) -> list:
+        if not self._has_trace:
+            return []
+        return [devmem.download(self.hbuf[k], self.n_own, self.dims[k]) if k else self._h0_host
+                for k in range(self.n_layers + 1)]
+
+    @property
+    def g(self) -> list:
+        if not self._has_grad:
+            return [None] * (self.n_layers + 1)
+        return [None] + [devmem.download(self.gext[k], self.n_own, self.dims[k]) for k in range(1, self.n_layers + 1)]
+
+    @property
+    def grad_weights(self) -> list:
+        """Allreduced ΔW^k of the last backward sweep (host copies; an extension:
+        the reference only exposes the updated weights)."""
+        if not self._has_grad:
+            return [None] * self.n_layers
+        return [devmem.download(self.dw_total[k], self.dims[k - 1], self.dims[k]) for k in range(1, self.n_layers + 1)]
+
+    @property
+    def weights(self) -> list:
+        ws = [devmem.download(self.w[k], self.dims[k - 1], self.dims[k]) for k in range(1, self.n_layers + 1)]
+        return _WeightList(self, ws)
+
+    @weights.setter
+    def weights(self, ws) -> None:
+        for k, w in enumerate(ws):
+            self._upload_weight(k, w)
+
+    def _upload_weight(self, k: int, w) -> None:
+        w = dense(w)
+        if w.shape != (self.dims[k], self.dims[k + 1]):
+            raise ValueError(f"W^{k + 1} has shape {w.shape}, expected {(self.dims[k], self.dims[k + 1])}")
+        self.w[k + 1][:, : self.dims[k + 1]].copy_(torch.from_numpy(w.astype(np.float32)))
+
+    @property
+    def a_fwd_local(self):
+        return self.layout.fwd.local_block()
+
+    @property
+    def a_fwd_recv(self) -> dict:
+        return {s: self.layout.fwd.recv_block(s) for s in self.layout.fwd.recv_from}
+
+    @property
+    def a_bwd_local(self):
+        return self.layout.bwd.local_block()
+
+    @property
+    def a_bwd_recv(self) -> dict:
+        return {s: self.layout.bwd.recv_block(s) for s in self.layout.bwd.recv_from}
+
+    # -- device step functions (shared by the in-process and distributed schedulers)
+    def stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def set_labels(self, labels) -> int:
+        """Upload this rank's label map; returns its labelled-row count."""
+        ids = np.asarray(labels.labeled_ids, dtype=np.int64)
+        lab = np.asarray(labels.labels, dtype=np.int64)
+        rows = self.global_rows
+        lab_map = np.full(max(self.n_own, 1), -1, dtype=np.int32)
+        if len(ids) and len(rows):
+            pos = np.searchsorted(rows, ids)
+            mine = (pos < len(rows)) & (rows[np.minimum(pos, len(rows) - 1)] == ids)
+            lab_map[pos[mine]] = lab[mine]
+            count = int(mine.sum())
+        else:
+            count = 0
+        self.label.copy_(torch.from_numpy(lab_map))
+        return count
+
+    def fwd_operand(self, k: int):
+        """(tensor, width) that layer k aggregates and exchanges."""
+        return self.xext[k], (self.dims[k] if self.transform_first[k] else self.dims[k - 1])
+
+    def fwd_transform(self, k: int) -> None:
+        """T^k = H^{k-1}·W^k into the own rows of the layer-k operand."""
+        if not self.transform_first[k] or self.n_own == 0:
+            return
+        x = self.hbuf[k - 1]
+        _lib.call("gcnb_dense_f32", x.data_ptr(), x.shape[1], self.n_own, self.dims[k - 1], self.w[k].data_ptr(),
+                  self.dims[k], self.xext[k].data_ptr(), self.xext[k].shape[1], self.stream())
+
+    def fwd_compute(self, k: int, rows: str = "all") -> None:
+        """runtime._fwd_compute for the selected own rows (all | interior | boundary)."""
+        op = self.op_fwd
+        sel, n_sel = self._rows(op, rows)
+        if n_sel == 0:
+            return
+        x, width = self.fwd_operand(k)
+        h = self.hbuf[k]
+        w = 0 if self.transform_first[k] else self.w[k].data_ptr()
+        _lib.call("gcnb_fwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(), op.csr.val.data_ptr(),
+                  sel, n_sel, x.data_ptr(), x.shape[1], width, w, self.dims[k], h.data_ptr(), h.shape[1],
+                  self.act, self.stream())
+
+    def loss_grad(self, inv_n_labeled: float) -> None:
+        """runtime._local_loss_grad: loss_sum and G^L for own rows."""
+        L = self.n_layers
+        h, g = self.hbuf[L], self.gext[L]
+        _lib.call("gcnb_loss_grad_f32", h.data_ptr(), h.shape[1], self.n_own, self.dims[L], self.label.data_ptr(),
+                  float(inv_n_labeled), g.data_ptr(), g.shape[1], self.act, self.loss_scratch.data_ptr(),
+                  self.loss_sum.data_ptr(), self.stream())
+
+    def bwd_compute(self, k: int, rows: str = "all", slot: int = 0) -> int:
+        """runtime._bwd_compute: G^{k-1} (k > 1) and ΔW^k partials; returns slots used."""
+        op = self.op_bwd
+        sel, n_sel = self._rows(op, rows)
+        gi, gb, ga = self.bwd_grids[k]
+        used = {"all": ga, "interior": gi, "boundary": gb}[rows]
+        g = self.gext[k]
+        hp = self.hbuf[k - 1]
+        gp = self.gext[k - 1] if k > 1 else None
+        part = self.partials[k][slot:]
+        _lib.call("gcnb_bwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(), op.csr.val.data_ptr(),
+                  sel, n_sel, g.data_ptr(), g.shape[1], self.dims[k], hp.data_ptr(), hp.shape[1],
+                  self.dims[k - 1], self.w[k].data_ptr(), 0 if gp is None else gp.data_ptr(),
+                  0 if gp is None else gp.shape[1], self.act, part.data_ptr(), self.stream())
+        return used
+
+    def reduce_dw(self, k: int, n_slots: int) -> None:
+        _lib.call("gcnb_reduce_partials_f32", self.partials[k].data_ptr(), n_slots, self.dw[k].numel(),
+                  self.dw[k].data_ptr(), 0, self.stream())
+
+    def sgd(self, k: int, dw: torch.Tensor) -> None:
+        _lib.call("gcnb_sgd_f32", self.w[k].data_ptr(), dw.data_ptr(), self.w[k].numel(),
+                  float(self.learning_rate), self.stream())
+
+    def _rows(self, op: _DeviceOp, rows: str):
+        if rows == "all":
+            return 0, self.n_own
+        t = op.interior if rows == "interior" else op.boundary
+        n = len(op.lay.interior) if rows == "interior" else len(op.lay.boundary)
+        return (t.data_ptr() if n else 0), n
+
+    def pack_to(self, phase: str, k: int, dst_bases: dict, flags=None, counter=None) -> None:
+        """Pack this rank's plan rows of the layer-k operand into each receiver's
+        halo (dst_bases[dst] = device pointer of the receiver's [own|halo] buffer
+        and its own-row count)."""
+        lay = self.layout.fwd if phase == "fwd" else self.layout.bwd
+        op = self.op_fwd if phase == "fwd" else self.op_bwd
+        if not lay.send_dst:
+            return
+        if phase == "fwd":
+            x, width = self.fwd_operand(k)
+        else:
+            x, width = self.gext[k], self.dims[k]
+        ld = x.shape[1]
+        dsts = []
+        for dst, slot in zip(lay.send_dst, lay.dst_slot):
+            base, n_dst = dst_bases[dst]
+            dsts.append(base + (n_dst + slot) * ld * 4)
+        _lib.call("gcnb_pack_rows_f32", x.data_ptr(), ld, width, op.send_idx.data_ptr(),
+                  _lib.int_array(lay.send_ptr), len(lay.send_dst), _lib.ptr_array(dsts), ld,
+                  None if flags is None else _lib.ptr_array(flags), counter, self.stream())
+
+
+# ---------------------------------------------------------------------------
+# scatter
+
+
+def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, device=None) -> list:
+    """Distribute row blocks per the partition and replicate the weights on the
+    device (runtime.py:233-275).  All ranks of this process share `device`."""
+    h0 = dense(h0)
+    if h0.shape != (a_hat.n_rows, model.dims[0]):
+        raise ValueError(f"h0 has shape {h0.shape}, expected ({a_hat.n_rows}, {model.dims[0]})")
+    dev = devmem.device(device)
+    plan_fwd = build_comm_plan(a_hat, pi, p)
+    if directed:
+        a_bwd = transpose_sparse(a_hat)
+        plan_bwd = build_comm_plan(a_bwd, pi, p)
+    else:
+        a_bwd, plan_bwd = a_hat, plan_fwd
+    states = []
+    for m in range(plan_fwd.p):
+        lay = build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, m)
+        states.append(ProcState(lay, plan_fwd, plan_bwd, model, h0[lay.global_rows], dev))
+    return states
+
+
+# ---------------------------------------------------------------------------
+# in-process schedule (all ranks on one device, one stream)
+
+
+def _bases(states, phase: str, k: int) -> dict:
+    out = {}
+    for st in states:
+        t = st.fwd_operand(k)[0] if phase == "fwd" else st.gext[k]
+        out[st.rank] = (t.data_ptr(), st.n_own)
+    return out
+
+
+def _log_phase(states, net, phase: str, k: int, epoch: int, step: int) -> None:
+    for st in states:
+        plan = st.plan_fwd if phase == "fwd" else st.plan_bwd
+        cols = st.dims[k - 1] if phase == "fwd" else st.dims[k]
+        width = st.fwd_operand(k)[1] if phase == "fwd" else st.dims[k]
+        for dst in range(plan.p):
+            rows = len(plan.send[st.rank][dst])
+            if rows and dst != st.rank:
+                _net_log(net, MessageRecord(epoch, step, phase, k, st.rank, dst, rows, cols,
+                                            nbytes=rows * devmem.ld_of(width) * 4))
+
+
+def _forward(states, net, epoch: int, step: int) -> None:
+    L = states[0].n_layers
+    for k in range(1, L + 1):
+        for st in states:
+            st.fwd_transform(k)
+        bases = _bases(states, "fwd", k)
+        for st in states:
+            st.pack_to("fwd", k, bases)
+        _log_phase(states, net, "fwd", k, epoch, step)
+        for st in states:
+            st.fwd_compute(k, "all")
+    for st in states:
+        st._has_trace = True
+
+
+def _backward(states, net, n_labeled: int, epoch: int, step: int, loss_out: torch.Tensor | None) -> None:
+    L = states[0].n_layers
+    inv = 1.0 / n_labeled if n_labeled else 0.0
+    for st in states:
+        st.loss_grad(inv)
+    if loss_out is not None:
+        _lib.call("gcnb_sum_buffers_f64", _lib.ptr_array([st.loss_sum.data_ptr() for st in states]), len(states), 1,
+                  loss_out.data_ptr(), states[0].stream())
+    for k in range(L, 0, -1):
+        bases = _bases(states, "bwd", k)
+        for st in states:
+            st.pack_to("bwd", k, bases)
+        _log_phase(states, net, "bwd", k, epoch, step)
+        for st in states:
+            used = st.bwd_compute(k, "all")
+            st.reduce_dw(k, used)
+    # allreduce_sum of every layer's ΔW in ascending rank order, then SGD on every replica
+    for k in range(1, L + 1):
+        total = states[0].dw[k]
+        if len(states) > 1:
+            total = states[0].dw_sum[k]
+            _lib.call("gcnb_sum_buffers_f32", _lib.ptr_array([st.dw[k].data_ptr() for st in states]), len(states),
+                      total.numel(), total.data_ptr(), states[0].stream())
+        for st in states:
+            st.dw_total[k] = total
+            st.sgd(k, total)
+    for st in states:
+        st._has_grad = True
+
+
+def _check_scheduler(scheduler: str) -> None:
+    if scheduler not in SCHEDULERS:
+        raise ValueError(f"unknown scheduler {scheduler!r}")
+
+
+def _check_device(states) -> None:
+    devs = {st.device for st in states}
+    if len(devs) != 1:
+        raise ValueError("in-process states must share one device; use distributed.py for one process per GPU")
+
+
+def _metrics_from_records(recs, p: int, wall: float, loss: float) -> EpochMetrics:
+    words = np.zeros(p, dtype=np.int64)
+    msgs = np.zeros(p, dtype=np.int64)
+    for r in recs:
+        words[r.src] += r.words
+        msgs[r.src] += 1
+    return EpochMetrics(int(words.sum()), int(words.max()) if p else 0, float(words.sum() / p) if p else 0.0,
+                        int(msgs.sum()), int(msgs.max()) if p else 0, wall, loss)
+
+
+def parallel_feedforward(states, net, scheduler: str = "round", epoch: int = 0):
+    """One forward pass over all layers (runtime.py:454-476)."""
+    _check_scheduler(scheduler)
+    _check_device(states)
+    with torch.cuda.device(states[0].device):
+        _forward(states, net, epoch, 0)
+    return states
+
+
+def parallel_backprop(states, net, labels, scheduler: str = "round", epoch: int = 0):
+    """Loss gradient, backward sweep, allreduced updates (runtime.py:479-518)."""
+    _check_scheduler(scheduler)
+    _check_device(states)
+    if not all(st._has_trace for st in states):
+        raise ValueError("run parallel_feedforward before parallel_backprop")
+    n_lab = len(labels)
+    if n_lab == 0:
+        raise ValueError("label set is empty")
+    dev = states[0].device
+    with torch.cuda.device(dev):
+        for st in states:
+            st.set_labels(labels)
+        loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        _backward(states, net, n_lab, epoch, 0, loss)
+        ev1.record()
+        ev1.synchronize()
+        wall = ev0.elapsed_time(ev1) / 1e3
+        loss_v = float(loss.item()) / n_lab
+    recs = [r for r in _net_records(net, epoch=epoch) if r.phase == "bwd"]
+    return states, _metrics_from_records(recs, len(states), wall, loss_v)
+
+
+def _run_step(states, net, labels, n_lab: int, epoch: int, step: int, loss_slot: torch.Tensor) -> None:
+    for st in states:
+        st.set_labels(labels)
+    _forward(states, net, epoch, step)
+    _backward(states, net, n_lab, epoch, step, loss_slot)
+
+
+def train_epochs(states, net, labels, epochs: int, mode=FullBatch(), scheduler: str = "round") -> list:
+    """Train for `epochs` epochs and return per-epoch metrics (runtime.py:565-632).
+
+    Losses stay on the device until the last epoch finishes (one sync per
+    call); `wallclock` is device time from CUDA events around each epoch."""
+    _check_scheduler(scheduler)
+    _check_device(states)
+    p = len(states)
+    dev = states[0].device
+    out = []
+    with torch.cuda.device(dev):
+        if isinstance(mode, FullBatch):
+            n_lab = len(labels)
+            if n_lab == 0:
+                raise ValueError("label set is empty")
+            if epochs <= 0:
+                return []
+            losses = torch.zeros(epochs, dtype=torch.float64, device=dev)
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(epochs + 1)]
+            for st in states:
+                st.set_labels(labels)
+            evs[0].record()
+            for e in range(epochs):
+                _forward(states, net, e, 0)
+                _backward(states, net, n_lab, e, 0, losses[e:e + 1])
+                evs[e + 1].record()
+            evs[-1].synchronize()
+            lv = (losses.cpu().numpy() / n_lab).tolist()
+            for e in range(epochs):
+                wall = evs[e].elapsed_time(evs[e + 1]) / 1e3
+                out.append(_metrics_from_records(_net_records(net, epoch=e), p, wall, lv[e]))
+            return out
+        return _train_minibatch(states, net, labels, epochs, mode, dev)
+
+
+def _local_labelset(labels, batch: np.ndarray):
+    ids = np.asarray(labels.labeled_ids, dtype=np.int64)
+    pos = np.searchsorted(batch, ids)
+    mine = (pos < len(batch)) & (batch[np.minimum(pos, len(batch) - 1)] == ids)
+    if not mine.any():
+        return None
+    return LabelSet(pos[mine], np.asarray(labels.labels)[mine], labels.n_classes)
+
+
+def _train_minibatch(states, net, labels, epochs: int, mode, dev) -> list:
+    """Mini-batch branch (runtime.py:593-632): per step a uniform sample
+    (rng [seed, 0x7B]), its induced renormalised sub-adjacency, a fresh plan and
+    scatter under the fixed owner array, one SGD step; weights persist."""
+    p = len(states)
+    rng = np.random.default_rng([int(mode.seed), 0x7B])
+    out = []
+    for e in range(epochs):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        losses = []
+        for step in range(mode.batches_per_epoch):
+            batch = np.sort(rng.choice(mode.adjacency.n_rows, size=mode.spec.batch_size, replace=False))
+            sub_hat = normalize_adjacency(induced_pattern(mode.adjacency, batch, add_diagonal=False),
+                                          add_self_loops=True)
+            st0 = states[0]
+            model = GcnModel(st0.dims, tuple(st0.weights), st0.activation, st0.learning_rate)
+            sub_states = scatter(sub_hat, np.asarray(mode.features)[batch], np.asarray(mode.owner)[batch], model,
+                                 directed=mode.directed, p=p, device=dev)
+            sub_labels = _local_labelset(labels, batch)
+            n_lab = len(sub_labels) if sub_labels is not None else 0
+            eff = sub_labels if sub_labels is not None else LabelSet(np.zeros(0, np.int64), np.zeros(0, np.int64),
+                                                                     labels.n_classes)
+            slot = torch.zeros(1, dtype=torch.float64, device=dev)
+            _run_step(sub_states, net, eff, n_lab, e, step, slot)
+            losses.append(float(slot.item()) / n_lab if n_lab else 0.0)
+            for st, sub in zip(states, sub_states):
+                for k in range(1, st.n_layers + 1):
+                    st.w[k].copy_(sub.w[k])
+        ev1.record()
+        ev1.synchronize()
+        wall = ev0.elapsed_time(ev1) / 1e3
+        out.append(_metrics_from_records(_net_records(net, epoch=e), p, wall,
+                                         float(np.mean(losses)) if losses else 0.0))
+    return out
