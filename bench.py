@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark: full-batch GCN training epoch time (BASELINE.json metric
+"GCN ms/epoch at 1/2/4/8 B200; SpMM HBM GB/s; halo bytes & exposed comm %").
+
+Default workload (N=1): BASELINE config[1] — 2-layer GCN (dims 16,16,8) on the
+amazon0601-shaped directed synthetic graph (403,394 vertices, 3,387,388 arcs).
+A *step* is one epoch: forward over both layers, loss, backward, ΔW
+allreduce and SGD update, all on the device.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload amazon0601|config1|roadnet|products]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   (one process per GPU)
+    python bench.py --impl reference ...   (the reference algorithm on host cores: oracle port)
+
+Timing (rejected otherwise): W >= 3 warm-up epochs; every timed epoch is
+preceded by an L2 flush (a 512 MiB write, outside the events); CUDA events on
+the launching stream; max over ranks; nvidia-smi clocks sampled during the
+timed region.  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GCN ms/epoch at 1/2/4/8 B200; SpMM HBM GB/s; halo bytes & exposed comm %"
+UNIT = "ms/epoch"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="amazon0601")
+    ap.add_argument("--partition", default="rp", choices=("rp", "hp"))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+
+def build_workload(name: str, seed: int):
+    import paper_2212_05009_b200 as gb
+    from paper_2212_05009_b200 import synth
+
+    gen, directed, dims = synth.WORKLOADS[name]
+    raw = gen(seed)
+    n = raw.n_rows
+    a_hat = gb.normalize_adjacency(raw)
+    rng_f = np.random.default_rng([seed, 0xFEA7])   # cli.py:148-151
+    h0 = rng_f.standard_normal((n, dims[0]))
+    rng_l = np.random.default_rng([seed, 0x1AB5])   # cli.py:154-159
+    count = max(1, round(0.1 * n))
+    ids = np.sort(rng_l.choice(n, size=count, replace=False))
+    labels = gb.LabelSet(ids, rng_l.integers(0, dims[-1], size=count), dims[-1])
+    model = gb.init_model(dims, seed)
+    return {"name": name, "raw": raw, "a_hat": a_hat, "h0": h0, "labels": labels, "model": model,
+            "directed": directed, "dims": dims, "n": n, "nnz": a_hat.nnz}
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({name for s in self.samples for name, v in zip(self.NAMES, s[2:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference algorithm; test infrastructure, timed only)
+
+
+def cpu_epoch_timer(wl, max_seconds: float = 20.0, max_epochs: int = 5, nthreads: int = 0):
+    from oracle import gcn_oracle as o
+
+    o.build()
+    threads = nthreads or o.max_threads()
+    a = o.as_csr(wl["a_hat"])
+    a_back = o.transpose(a) if wl["directed"] else a
+    ws = [np.asarray(w) for w in wl["model"].weights]
+    ids, y = wl["labels"].labeled_ids, wl["labels"].labels
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < max_epochs and (time.perf_counter() - t_all) < max_seconds:
+        t0 = time.perf_counter()
+        ws, _, _ = _oracle_one_epoch(o, ws, a, a_back, wl["h0"], ids, y, wl["model"].learning_rate, threads)
+        times.append(time.perf_counter() - t0)
+    return times, threads
+
+
+def _oracle_one_epoch(o, ws, a, a_back, h0, ids, y, lr, threads):
+    z, h = o.serial_forward(a, ws, h0, nthreads=threads)
+    loss, grad = o.nll_and_grad(h[-1], ids, y)
+    dws, _ = o.serial_backward(a_back, ws, z, h, grad, nthreads=threads)
+    return [w - lr * dw for w, dw in zip(ws, dws)], loss, None
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    wl = build_workload(args.workload, args.seed)
+    from oracle import gcn_oracle as o
+
+    o.build()
+    threads = o.max_threads()
+    a = o.as_csr(wl["a_hat"])
+    a_back = o.transpose(a) if wl["directed"] else a
+    ws = [np.asarray(w) for w in wl["model"].weights]
+    ids, y = wl["labels"].labeled_ids, wl["labels"].labels
+    for _ in range(args.warmup):
+        ws, _, _ = _oracle_one_epoch(o, ws, a, a_back, wl["h0"], ids, y, wl["model"].learning_rate, threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ws, _, _ = _oracle_one_epoch(o, ws, a, a_back, wl["h0"], ids, y, wl["model"].learning_rate, threads)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(times))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(ms, 4), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["name"], "n": wl["n"], "nnz_ahat": wl["nnz"], "dims": list(wl["dims"]),
+                   "directed": wl["directed"], "partition": "none (p=1 serial oracle)"},
+        "cpu_baseline": {"value": round(ms, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full epochs of the fp64 oracle port (oracle/gcn_oracle.py + "
+                                   f"oracle.c, OpenMP {threads} threads) after {args.warmup} warm-up epochs"},
+        "e2e": {"value": round(ms, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU, single process
+
+
+def roofline_summary(kernel_rows, peak, peak_kind, steps):
+    """Pick the kernel with the largest time share; achieved = algorithmic bytes / mean launch time."""
+    agg = {}
+    for name, algo, flops, ms in kernel_rows:
+        e = agg.setdefault(name, [0, 0, 0.0, 0])
+        e[0] += algo
+        e[1] += flops
+        e[2] += ms
+        e[3] += 1
+    total_ms = sum(v[2] for v in agg.values())
+    name, (algo, flops, ms, cnt) = max(agg.items(), key=lambda kv: kv[1][2])
+    mean_ms = ms / cnt
+    achieved = (algo / cnt) / (mean_ms * 1e-3) / 1e9
+    table = {k: {"ms_per_launch": round(v[2] / v[3], 5), "launches": v[3] // max(steps, 1),
+                 "algo_bytes": v[0] // v[3], "gbs": round((v[0] / v[3]) / (v[2] / v[3] * 1e-3) / 1e9, 1)
+                 if v[2] > 0 else None, "share": round(v[2] / total_ms, 4)} for k, v in sorted(agg.items())}
+    return name, achieved, mean_ms, algo // cnt, table
+
+
+def traffic_for(workload: str, kernel: str):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(workload, {}).get(kernel)
+    return None
+
+
+def run_single(args):
+    import torch
+
+    import paper_2212_05009_b200 as gb
+    from paper_2212_05009_b200 import _lib, profiling
+    from paper_2212_05009_b200.runtime import EpochRunner
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    wl = build_workload(args.workload, args.seed)
+    n = wl["n"]
+    owner = np.zeros(n, dtype=np.int64)
+    states = gb.scatter(wl["a_hat"], wl["h0"], owner, wl["model"], directed=wl["directed"], p=1, device=dev)
+    runner = EpochRunner(states, wl["labels"])
+
+    c0 = _lib.launch_count()
+    runner.enqueue()
+    torch.cuda.synchronize()
+    launches_per_epoch = _lib.launch_count() - c0
+    for _ in range(max(args.warmup - 1, 0)):
+        runner.enqueue()
+    torch.cuda.synchronize()
+
+    timer = profiling.KernelTimer()
+    if not args.no_graph:
+        runner.capture(timer)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kernel_rows = []
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clocks:
+        for i in range(args.steps):
+            flush.zero_()
+            ev0[i].record()
+            if args.no_graph:
+                with profiling.active(timer):
+                    timer.spans.clear()
+                    runner.enqueue()
+            else:
+                runner.replay()
+            ev1[i].record()
+            ev1[i].synchronize()
+            kernel_rows.extend(timer.results())
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    ms = float(np.mean(step_ms))
+
+    # end to end through the public API: pinned host features -> device, one
+    # train_epochs call (labels upload, forward, loss, backward, SGD, loss D2H)
+    net = gb.DeviceNetwork(1)
+    d0 = wl["dims"][0]
+    h0_pinned = torch.from_numpy(wl["h0"].astype(np.float32)).pin_memory()
+    e2e_times = []
+    for i in range(max(3, min(args.steps, 20))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        states[0].hbuf[0][:, :d0].copy_(h0_pinned, non_blocking=True)
+        m = gb.train_epochs(states, net, wl["labels"], 1)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_ms = 1e3 * float(np.mean(e2e_times))
+    h2d = int(h0_pinned.numel() * 4 + n * 4)  # features + label map
+    d2h = 8 * 1  # the epoch loss
+
+    peak, peak_kind = measured_peaks()
+    kname, achieved, kms, kbytes, table = roofline_summary(kernel_rows, peak, peak_kind, args.steps)
+    cpu_times, cpu_threads = cpu_epoch_timer(wl)
+    cpu_ms = 1e3 * float(np.mean(cpu_times))
+    clk = clocks.summary()
+    line = {
+        "metric": METRIC, "value": round(ms, 4), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl["name"], "n": n, "nnz_ahat": wl["nnz"], "dims": list(wl["dims"]),
+                   "directed": wl["directed"], "partition": "p=1", "l2": "flushed (512 MiB write) before every step",
+                   "graph": not args.no_graph, "seed": args.seed},
+        "e2e": {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "loss_last": m[0].loss},
+        "gpu_launches": int(launches_per_epoch * args.steps),
+        "roofline": {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic_for(wl["name"], kname), "algo_bytes_per_launch": kbytes,
+                     "ms_per_launch": round(kms, 5)},
+        "kernels": table,
+        "halo_bytes_per_epoch": 0, "exposed_comm_pct": 0.0,
+        "cpu_baseline": {"value": round(cpu_ms, 3), "unit": UNIT, "cores": cpu_threads, "kind": "port",
+                         "sample": f"{len(cpu_times)} full fp64 epochs of the oracle port (OpenMP {cpu_threads} "
+                                   f"threads) on the same graph"},
+        "clocks": clk,
+    }
+    timer.close()
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2212_05009_b200 import distributed
+
+        return distributed.bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summary,
+                                      cpu_epoch_timer, METRIC, UNIT)
+    return run_single(args)
+
+
+if __name__ == "__main__":
+    main()

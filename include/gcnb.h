@@ -63,6 +63,15 @@ int gcnb_ipc_open_handle(const uint8_t handle[64], void** dptr_out);
 int gcnb_ipc_close_handle(void* dptr);
 int gcnb_enable_peer_access(int peer_device);
 
+/* ---- timing events (usable inside CUDA-graph capture: external = 1 records
+ * an external event node, so per-kernel spans can be timed on graph replay) */
+int gcnb_event_create(void** ev);
+int gcnb_event_destroy(void* ev);
+int gcnb_event_record(void* ev, void* stream, int32_t external);
+int gcnb_event_elapsed_ms(void* ev0, void* ev1, float* ms_out);
+/* 1 if `stream` is currently capturing a CUDA graph */
+int gcnb_stream_is_capturing(void* stream, int32_t* out);
+
 /* ---- L1 kernels: sparse.py --------------------------------------------- */
 
 /* sparse.spmm (sparse.py:196-207): Y[r] = Σ_j A[r,j]·X[j] for r = rows[i]

@@ -37,6 +37,11 @@ _SIGNATURES = {
     "gcnb_ipc_open_handle": (_c_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "gcnb_ipc_close_handle": (_c_int, [_vp]),
     "gcnb_enable_peer_access": (_c_int, [_c_int]),
+    "gcnb_event_create": (_c_int, [ctypes.POINTER(_vp)]),
+    "gcnb_event_destroy": (_c_int, [_vp]),
+    "gcnb_event_record": (_c_int, [_vp, _vp, _c_int]),
+    "gcnb_event_elapsed_ms": (_c_int, [_vp, _vp, ctypes.POINTER(_f32)]),
+    "gcnb_stream_is_capturing": (_c_int, [_vp, ctypes.POINTER(_c_int)]),
     "gcnb_spmm_f32": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp]),
     "gcnb_pack_rows_f32": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _vp, _c_int, _vp, _vp, _vp]),
     "gcnb_wait_flags": (_c_int, [_vp, _vp, _c_int, _vp, _vp, _c_int, _vp]),

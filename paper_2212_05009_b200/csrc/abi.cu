@@ -121,3 +121,41 @@ extern "C" int gcnb_enable_peer_access(int peer_device) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
   return GCNB_OK;
 }
+
+extern "C" int gcnb_event_create(void** ev) {
+  GCNB_REQUIRE(ev != nullptr, "event create: null output");
+  cudaError_t e = cudaEventCreate(reinterpret_cast<cudaEvent_t*>(ev));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_event_destroy(void* ev) {
+  if (!ev) return GCNB_OK;
+  cudaError_t e = cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventDestroy");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_event_record(void* ev, void* stream, int32_t external) {
+  GCNB_REQUIRE(ev != nullptr, "event record: null event");
+  cudaError_t e = cudaEventRecordWithFlags(reinterpret_cast<cudaEvent_t>(ev), (cudaStream_t)stream,
+                                           external ? cudaEventRecordExternal : cudaEventRecordDefault);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecordWithFlags");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_event_elapsed_ms(void* ev0, void* ev1, float* ms_out) {
+  GCNB_REQUIRE(ev0 && ev1 && ms_out, "event elapsed: null arguments");
+  cudaError_t e = cudaEventElapsedTime(ms_out, reinterpret_cast<cudaEvent_t>(ev0), reinterpret_cast<cudaEvent_t>(ev1));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventElapsedTime");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_stream_is_capturing(void* stream, int32_t* out) {
+  GCNB_REQUIRE(out != nullptr, "stream capture status: null output");
+  cudaStreamCaptureStatus st;
+  cudaError_t e = cudaStreamIsCapturing((cudaStream_t)stream, &st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamIsCapturing");
+  *out = st == cudaStreamCaptureStatusActive ? 1 : 0;
+  return GCNB_OK;
+}

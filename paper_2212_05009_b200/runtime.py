@@ -35,6 +35,7 @@ from ._lib import CommError
 from .comm import CommPlan, build_comm_plan
 from .host import GcnModel, LabelSet, MiniBatchSpec, induced_pattern
 from .layout import OpLayout, RankLayout, build_rank_layout
+from .profiling import span
 from .sparse import dense, normalize_adjacency, transpose_sparse
 
 SCHEDULERS = ("round", "threads")
@@ -176,6 +177,12 @@ class _DeviceOp:
         self.interior = devmem.upload_index(lay.interior, dev)
         self.boundary = devmem.upload_index(lay.boundary, dev)
         self.send_idx = devmem.upload_index(lay.send_idx, dev)
+        lens = np.diff(lay.row_ptr)
+        self._nnz = {"all": int(lay.row_ptr[-1]), "interior": int(lens[lay.interior].sum()),
+                     "boundary": int(lens[lay.boundary].sum())}
+
+    def nnz_of(self, rows: str) -> int:
+        return self._nnz[rows]
 
 
 class _WeightList(list):
@@ -213,6 +220,7 @@ class ProcState:
         self._h0_host = np.ascontiguousarray(h0)
         self._has_trace = False
         self._has_grad = False
+        self.n_labeled = 0
         L = self.n_layers
         n = len(layout.global_rows)
         self.n_own = n
@@ -337,6 +345,7 @@ class ProcState:
         else:
             count = 0
         self.label.copy_(torch.from_numpy(lab_map))
+        self.n_labeled = count
         return count
 
     def fwd_operand(self, k: int):
@@ -348,8 +357,10 @@ class ProcState:
         if not self.transform_first[k] or self.n_own == 0:
             return
         x = self.hbuf[k - 1]
-        _lib.call("gcnb_dense_f32", x.data_ptr(), x.shape[1], self.n_own, self.dims[k - 1], self.w[k].data_ptr(),
-                  self.dims[k], self.xext[k].data_ptr(), self.xext[k].shape[1], self.stream())
+        n, a, b = self.n_own, self.dims[k - 1], self.dims[k]
+        with span(f"dense{k}", 4 * (n * a + a * b + n * b), 2 * n * a * b, self.stream()):
+            _lib.call("gcnb_dense_f32", x.data_ptr(), x.shape[1], n, a, self.w[k].data_ptr(), b,
+                      self.xext[k].data_ptr(), self.xext[k].shape[1], self.stream())
 
     def fwd_compute(self, k: int, rows: str = "all") -> None:
         """runtime._fwd_compute for the selected own rows (all | interior | boundary)."""
@@ -359,18 +370,29 @@ class ProcState:
             return
         x, width = self.fwd_operand(k)
         h = self.hbuf[k]
-        w = 0 if self.transform_first[k] else self.w[k].data_ptr()
-        _lib.call("gcnb_fwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(), op.csr.val.data_ptr(),
-                  sel, n_sel, x.data_ptr(), x.shape[1], width, w, self.dims[k], h.data_ptr(), h.shape[1],
-                  self.act, self.stream())
+        fused = not self.transform_first[k]
+        w = self.w[k].data_ptr() if fused else 0
+        nnz = op.nnz_of(rows)
+        d_out = self.dims[k]
+        algo = 4 * (n_sel + 1) + 8 * nnz + 4 * width * nnz + 4 * d_out * n_sel
+        flops = 2 * nnz * width
+        if fused:
+            algo += 4 * width * d_out
+            flops += 2 * n_sel * width * d_out
+        with span(f"fwd{k}", algo, flops, self.stream()):
+            _lib.call("gcnb_fwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
+                      op.csr.val.data_ptr(), sel, n_sel, x.data_ptr(), x.shape[1], width, w, d_out, h.data_ptr(),
+                      h.shape[1], self.act, self.stream())
 
     def loss_grad(self, inv_n_labeled: float) -> None:
         """runtime._local_loss_grad: loss_sum and G^L for own rows."""
         L = self.n_layers
         h, g = self.hbuf[L], self.gext[L]
-        _lib.call("gcnb_loss_grad_f32", h.data_ptr(), h.shape[1], self.n_own, self.dims[L], self.label.data_ptr(),
-                  float(inv_n_labeled), g.data_ptr(), g.shape[1], self.act, self.loss_scratch.data_ptr(),
-                  self.loss_sum.data_ptr(), self.stream())
+        d = self.dims[L]
+        with span("loss", 4 * self.n_own + 4 * d * (self.n_labeled + self.n_own), 0, self.stream()):
+            _lib.call("gcnb_loss_grad_f32", h.data_ptr(), h.shape[1], self.n_own, d, self.label.data_ptr(),
+                      float(inv_n_labeled), g.data_ptr(), g.shape[1], self.act, self.loss_scratch.data_ptr(),
+                      self.loss_sum.data_ptr(), self.stream())
 
     def bwd_compute(self, k: int, rows: str = "all", slot: int = 0) -> int:
         """runtime._bwd_compute: G^{k-1} (k > 1) and ΔW^k partials; returns slots used."""
@@ -382,19 +404,31 @@ class ProcState:
         hp = self.hbuf[k - 1]
         gp = self.gext[k - 1] if k > 1 else None
         part = self.partials[k][slot:]
-        _lib.call("gcnb_bwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(), op.csr.val.data_ptr(),
-                  sel, n_sel, g.data_ptr(), g.shape[1], self.dims[k], hp.data_ptr(), hp.shape[1],
-                  self.dims[k - 1], self.w[k].data_ptr(), 0 if gp is None else gp.data_ptr(),
-                  0 if gp is None else gp.shape[1], self.act, part.data_ptr(), self.stream())
+        nnz = op.nnz_of(rows)
+        dk, dp = self.dims[k], self.dims[k - 1]
+        algo = 4 * (n_sel + 1) + 8 * nnz + 4 * dk * nnz + 4 * dp * n_sel + 4 * dp * dk * used
+        flops = 2 * nnz * dk + 2 * n_sel * dp * dk
+        if gp is not None:
+            algo += 4 * dp * n_sel + 4 * dp * dk
+            flops += 2 * n_sel * dp * dk
+        with span(f"bwd{k}", algo, flops, self.stream()):
+            _lib.call("gcnb_bwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
+                      op.csr.val.data_ptr(), sel, n_sel, g.data_ptr(), g.shape[1], dk, hp.data_ptr(), hp.shape[1],
+                      dp, self.w[k].data_ptr(), 0 if gp is None else gp.data_ptr(),
+                      0 if gp is None else gp.shape[1], self.act, part.data_ptr(), self.stream())
         return used
 
     def reduce_dw(self, k: int, n_slots: int) -> None:
-        _lib.call("gcnb_reduce_partials_f32", self.partials[k].data_ptr(), n_slots, self.dw[k].numel(),
-                  self.dw[k].data_ptr(), 0, self.stream())
+        size = self.dw[k].numel()
+        with span(f"reduce{k}", 4 * size * (n_slots + 1), size * n_slots, self.stream()):
+            _lib.call("gcnb_reduce_partials_f32", self.partials[k].data_ptr(), n_slots, size,
+                      self.dw[k].data_ptr(), 0, self.stream())
 
     def sgd(self, k: int, dw: torch.Tensor) -> None:
-        _lib.call("gcnb_sgd_f32", self.w[k].data_ptr(), dw.data_ptr(), self.w[k].numel(),
-                  float(self.learning_rate), self.stream())
+        size = self.w[k].numel()
+        with span(f"sgd{k}", 12 * size, 2 * size, self.stream()):
+            _lib.call("gcnb_sgd_f32", self.w[k].data_ptr(), dw.data_ptr(), size, float(self.learning_rate),
+                      self.stream())
 
     def _rows(self, op: _DeviceOp, rows: str):
         if rows == "all":
@@ -420,9 +454,11 @@ class ProcState:
         for dst, slot in zip(lay.send_dst, lay.dst_slot):
             base, n_dst = dst_bases[dst]
             dsts.append(base + (n_dst + slot) * ld * 4)
-        _lib.call("gcnb_pack_rows_f32", x.data_ptr(), ld, width, op.send_idx.data_ptr(),
-                  _lib.int_array(lay.send_ptr), len(lay.send_dst), _lib.ptr_array(dsts), ld,
-                  None if flags is None else _lib.ptr_array(flags), counter, self.stream())
+        r = int(lay.send_ptr[-1])
+        with span(f"pack_{phase}{k}", 8 * width * r + 4 * r, 0, self.stream()):
+            _lib.call("gcnb_pack_rows_f32", x.data_ptr(), ld, width, op.send_idx.data_ptr(),
+                      _lib.int_array(lay.send_ptr), len(lay.send_dst), _lib.ptr_array(dsts), ld,
+                      None if flags is None else _lib.ptr_array(flags), counter, self.stream())
 
 
 # ---------------------------------------------------------------------------
@@ -462,6 +498,8 @@ def _bases(states, phase: str, k: int) -> dict:
 
 
 def _log_phase(states, net, phase: str, k: int, epoch: int, step: int) -> None:
+    if net is None:
+        return
     for st in states:
         plan = st.plan_fwd if phase == "fwd" else st.plan_bwd
         cols = st.dims[k - 1] if phase == "fwd" else st.dims[k]
@@ -516,6 +554,56 @@ def _backward(states, net, n_labeled: int, epoch: int, step: int, loss_out: torc
             st.sgd(k, total)
     for st in states:
         st._has_grad = True
+
+
+class EpochRunner:
+    """One full-batch epoch of in-process states as a pure device sequence
+    (no host syncs, no allocations), so it can be replayed as a CUDA graph.
+
+    `enqueue()` issues the epoch on the current stream; `capture()` records it
+    into a CUDA graph (optionally with per-kernel timing spans) and `replay()`
+    launches that graph.  Message accounting is left to the caller (the plan
+    makes it static: see `log_epoch`)."""
+
+    def __init__(self, states, labels):
+        _check_device(states)
+        self.states = states
+        self.dev = states[0].device
+        self.n_lab = len(labels)
+        if self.n_lab == 0:
+            raise ValueError("label set is empty")
+        with torch.cuda.device(self.dev):
+            for st in states:
+                st.set_labels(labels)
+            self.loss = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.graph = None
+
+    def enqueue(self) -> None:
+        with torch.cuda.device(self.dev):
+            _forward(self.states, None, 0, 0)
+            _backward(self.states, None, self.n_lab, 0, 0, self.loss)
+
+    def capture(self, timer=None) -> None:
+        from . import profiling
+
+        with torch.cuda.device(self.dev):
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with profiling.active(timer):
+                with torch.cuda.graph(g, capture_error_mode="relaxed"):
+                    _forward(self.states, None, 0, 0)
+                    _backward(self.states, None, self.n_lab, 0, 0, self.loss)
+            self.graph = g
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+    def log_epoch(self, net, epoch: int, step: int = 0) -> None:
+        L = self.states[0].n_layers
+        for k in range(1, L + 1):
+            _log_phase(self.states, net, "fwd", k, epoch, step)
+        for k in range(L, 0, -1):
+            _log_phase(self.states, net, "bwd", k, epoch, step)
 
 
 def _check_scheduler(scheduler: str) -> None:

@@ -1,0 +1,119 @@
+"""Seeded synthetic graphs of the BASELINE.json shapes (no datasets are reachable offline).
+
+Edge-count convention: each generator produces exactly the
+dataset's stored nonzeros of A; Â later adds n self loops.  Every generator
+is deterministic in `seed` and documented in BASELINE.md §4 / DESIGN.md §6.
+
+* config1  — gcnpart's tests/helpers.random_undirected(10_000, 0.001, 0)
+             (helpers.py:67-71), drawn in row chunks (same rng stream,
+             bounded memory): 100,010 stored nonzeros.
+* amazon0601 — directed, 403,394 vertices, exactly 3,387,388 arcs: per-vertex
+             out-degree ~ Poisson, 90 % of targets at a two-sided geometric
+             ring offset (mean 50), 10 % uniform shortcuts, then a seeded
+             random relabelling (destroys index locality, keeps graph locality).
+* roadnet  — undirected 1404×1404 lattice (1,971,216 vertices) keeping exactly
+             2,766,607 of its edges (5,533,214 stored nonzeros), relabelled.
+* products — undirected degree-corrected SBM, 2,449,029 vertices, exactly
+             61,859,140 pairs (123,718,280 stored nonzeros), 2,048 blocks,
+             80 % intra-block pairs, log-normal degree propensities, relabelled.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .sparse import CsrMatrix
+
+
+def _csr_from_pairs(n: int, rows: np.ndarray, cols: np.ndarray) -> CsrMatrix:
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
+    return CsrMatrix(n, n, rp, cols, np.ones(len(cols)))
+
+
+def _exact_count(keys: np.ndarray, m: int, rng) -> np.ndarray:
+    keys = np.unique(keys)
+    if len(keys) < m:
+        raise RuntimeError(f"generator produced {len(keys)} distinct entries, need {m}")
+    return np.sort(keys[rng.choice(len(keys), size=m, replace=False)])
+
+
+def config1(seed: int = 0, n: int = 10_000, density: float = 0.001) -> CsrMatrix:
+    rng = np.random.default_rng([seed, 0xD1])
+    rows, cols = [], []
+    chunk = 1000
+    for r0 in range(0, n, chunk):
+        blk = rng.random((min(chunk, n - r0), n)) < density
+        r, c = np.nonzero(blk)
+        r = r + r0
+        keep = c > r  # strict upper triangle (np.triu(..., 1))
+        rows.append(r[keep])
+        cols.append(c[keep])
+    r = np.concatenate(rows)
+    c = np.concatenate(cols)
+    return _csr_from_pairs(n, np.concatenate([r, c]), np.concatenate([c, r]))
+
+
+def amazon0601(seed: int = 0, n: int = 403_394, m: int = 3_387_388, mean_offset: float = 50.0,
+               shortcut: float = 0.10) -> CsrMatrix:
+    rng = np.random.default_rng([seed, 0xA0601])
+    deg = rng.poisson(1.03 * m / n, n)
+    src = np.repeat(np.arange(n, dtype=np.int64), deg)
+    k = len(src)
+    off = rng.geometric(1.0 / mean_offset, k) * np.where(rng.random(k) < 0.5, -1, 1)
+    dst = np.where(rng.random(k) < shortcut, rng.integers(0, n, k), (src + off) % n)
+    keep = dst != src
+    keys = _exact_count(src[keep] * n + dst[keep], m, rng)
+    perm = rng.permutation(n)
+    return _csr_from_pairs(n, perm[keys // n], perm[keys % n])
+
+
+def roadnet(seed: int = 0, side: int = 1404, kept_edges: int = 2_766_607) -> CsrMatrix:
+    rng = np.random.default_rng([seed, 0x20AD])
+    n = side * side
+    v = np.arange(n, dtype=np.int64).reshape(side, side)
+    horiz = np.stack([v[:, :-1].ravel(), v[:, 1:].ravel()], axis=1)
+    vert = np.stack([v[:-1, :].ravel(), v[1:, :].ravel()], axis=1)
+    edges = np.concatenate([horiz, vert])
+    edges = edges[np.sort(rng.choice(len(edges), size=kept_edges, replace=False))]
+    perm = rng.permutation(n)
+    u, w = perm[edges[:, 0]], perm[edges[:, 1]]
+    return _csr_from_pairs(n, np.concatenate([u, w]), np.concatenate([w, u]))
+
+
+def products(seed: int = 0, n: int = 2_449_029, pairs: int = 61_859_140, blocks: int = 2048,
+             intra: float = 0.8, sigma: float = 1.0) -> CsrMatrix:
+    rng = np.random.default_rng([seed, 0x9200])
+    block = np.sort(rng.integers(0, blocks, n))          # contiguous blocks before relabelling
+    bounds = np.searchsorted(block, np.arange(blocks + 1))
+    prop = rng.lognormal(0.0, sigma, n)
+    cum = np.cumsum(prop)
+    k = int(pairs * 1.04)
+    u = np.minimum(np.searchsorted(cum, rng.random(k) * cum[-1]), n - 1)
+    same = rng.random(k) < intra
+    # intra-block partner: inverse-CDF draw restricted to u's block
+    lo = bounds[block[u]]
+    hi = bounds[block[u] + 1]
+    c_lo = np.where(lo > 0, cum[lo - 1], 0.0)
+    c_hi = cum[hi - 1]
+    w_in = np.minimum(np.searchsorted(cum, c_lo + rng.random(k) * (c_hi - c_lo)), n - 1)
+    w_any = np.minimum(np.searchsorted(cum, rng.random(k) * cum[-1]), n - 1)
+    w = np.where(same, w_in, w_any)
+    keep = u != w
+    a, b = np.minimum(u[keep], w[keep]), np.maximum(u[keep], w[keep])
+    keys = _exact_count(a * n + b, pairs, rng)
+    perm = rng.permutation(n)
+    x, y = perm[keys // n], perm[keys % n]
+    return _csr_from_pairs(n, np.concatenate([x, y]), np.concatenate([y, x]))
+
+
+WORKLOADS = {
+    # name: (generator, directed, dims)
+    "config1": (config1, False, (16, 16, 8)),
+    "amazon0601": (amazon0601, True, (16, 16, 8)),
+    "roadnet": (roadnet, False, (16, 16, 8)),
+    "products": (products, False, (100, 128, 47)),
+    "products3": (products, False, (100, 128, 128, 47)),
+}
