@@ -147,6 +147,10 @@ int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* 
  * summed in slot order (fixed), j < size. */
 int gcnb_reduce_partials_f32(const float* partials, int32_t n_slots, int64_t size,
                              float* out, int32_t accumulate, void* stream);
+/* The same reduction with the SGD step of runtime._apply_update
+ * (runtime.py:359-360) fused: out = ΔW, then w -= lr·out.  size % 4 == 0. */
+int gcnb_reduce_sgd_f32(const float* partials, int32_t n_slots, int64_t size,
+                        float* out, int32_t accumulate, float* w, float lr, void* stream);
 
 /* runtime._local_loss_grad (runtime.py:309-333): for every own row r < n_rows,
  * label[r] >= 0 marks a labelled row of class label[r].  For labelled rows:

@@ -54,6 +54,7 @@ _SIGNATURES = {
         [_vp, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp,
          _vp]),
     "gcnb_reduce_partials_f32": (_c_int, [_vp, _c_int, _c_i64, _vp, _c_int, _vp]),
+    "gcnb_reduce_sgd_f32": (_c_int, [_vp, _c_int, _c_i64, _vp, _c_int, _vp, _f32, _vp]),
     "gcnb_loss_scratch_doubles": (_c_int, []),
     "gcnb_loss_grad_f32": (
         _c_int, [_vp, _c_int, _c_int, _c_int, _vp, _f64, _vp, _c_int, _c_int, _vp, _vp, _vp]),

@@ -94,42 +94,84 @@ __global__ void k_wait(const unsigned long long* flags, WaitArgs a, unsigned lon
   }
 }
 
-// One warp per own row.  label[r] >= 0 marks a labelled row.
+// label[r] >= 0 marks a labelled own row.
 constexpr int LOSS_BLOCKS_MAX = 148 * 8;
 
-__global__ void __launch_bounds__(NT) k_loss(const float* __restrict__ H, int ldh, int n_rows, int d,
-                                             const int* __restrict__ label, double inv_n, float* __restrict__ G,
-                                             int ldg, int act, double* __restrict__ partials) {
+// A group of LPR lanes owns a row; each lane owns VPL float4 column chunks
+// (one 16-byte load/store each).  Unlabelled rows write zeros without reading
+// H.  All lanes of a warp run the group shuffles (warp-uniform loop).
+__device__ __forceinline__ float f4get(const float4& v, int e) {
+  return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(NT) k_loss(const float4* __restrict__ H4, int ldh4, int n_rows, int d,
+                                             const int* __restrict__ label, double inv_n, float4* __restrict__ G4,
+                                             int ldg4, int act, double* __restrict__ partials) {
+  constexpr int GPW = 32 / LPR;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  const int gl = lane & (LPR - 1), gw = lane / LPR;
+  const int c4 = (d + 3) / 4;
+  const float inv = (float)inv_n;
   double local = 0.0;
-  for (int row = blockIdx.x * WARPS + warp; row < n_rows; row += gridDim.x * WARPS) {
-    const int y = __ldg(label + row);
-    float* g = G + (size_t)row * ldg;
+  const int warp_global = blockIdx.x * WARPS + warp;
+  for (int row0 = warp_global * GPW; row0 < n_rows; row0 += gridDim.x * WARPS * GPW) {
+    const int row = row0 + gw;
+    const int y = row < n_rows ? __ldg(label + row) : -1;
+    float4 hv[VPL];
+    float m = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int ch = gl + q * LPR;
+      hv[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (y >= 0 && ch < c4) {
+        hv[q] = __ldg(H4 + (size_t)row * ldh4 + ch);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (4 * ch + e < d) m = fmaxf(m, f4get(hv[q], e));
+      }
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o, LPR));
+    float s = 0.0f;
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int ch = gl + q * LPR;
+      if (y >= 0 && ch < c4) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (4 * ch + e < d) s += expf(f4get(hv[q], e) - m);
+      }
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, LPR);
+    if (row >= n_rows) continue;
+    float4* g = G4 + (size_t)row * ldg4;
     if (y < 0) {
-      for (int j = lane; j < ldg; j += 32) g[j] = 0.0f;
+      for (int ch = gl; ch < ldg4; ch += LPR) g[ch] = make_float4(0.f, 0.f, 0.f, 0.f);
       continue;
     }
-    const float* h = H + (size_t)row * ldh;
-    float m = -INFINITY;
-    for (int j = lane; j < d; j += 32) m = fmaxf(m, h[j]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    float s = 0.0f;
-    for (int j = lane; j < d; j += 32) s += expf(h[j] - m);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const float lse = logf(s);
-    for (int j = lane; j < ldg; j += 32) {
-      float gj = 0.0f;
-      if (j < d) {
-        const float hj = h[j];
-        const float logp = (hj - m) - lse;
-        if (j == y) local -= (double)logp;
-        gj = (expf(logp) - (j == y ? 1.0f : 0.0f)) * (float)inv_n * act_grad_from_h(hj, act);
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int ch = gl + q * LPR;
+      if (ch >= ldg4) continue;
+      float o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = 4 * ch + e;
+        o[e] = 0.0f;
+        if (j < d) {
+          const float hj = f4get(hv[q], e);
+          const float logp = (hj - m) - lse;
+          if (j == y) local -= (double)logp;
+          o[e] = (expf(logp) - (j == y ? 1.0f : 0.0f)) * inv * act_grad_from_h(hj, act);
+        }
       }
-      g[j] = gj;
+      g[ch] = make_float4(o[0], o[1], o[2], o[3]);
     }
+    for (int ch = gl + VPL * LPR; ch < ldg4; ch += LPR) g[ch] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   // fixed-order block reduction of the per-lane NLL sums
 #pragma unroll
@@ -144,12 +186,13 @@ __global__ void __launch_bounds__(NT) k_loss(const float* __restrict__ H, int ld
   }
 }
 
+// One warp: lane-strided partial sums, then a fixed xor tree (deterministic).
 __global__ void k_sum_partials_f64(const double* __restrict__ partials, int n, double* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < n; ++i) t += partials[i];
-    *out = t;
-  }
+  double t = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) t += partials[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (threadIdx.x == 0) *out = t;
 }
 
 struct PtrArgsF {
@@ -258,10 +301,23 @@ extern "C" int gcnb_loss_grad_f32(const float* h, int32_t ldh, int32_t n_rows, i
   GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "loss: unknown activation %d", act);
   GCNB_REQUIRE(scratch && loss_sum, "loss: scratch and loss_sum required");
   GCNB_REQUIRE(n_rows == 0 || (h && g && label), "loss: null operands");
+  GCNB_REQUIRE(d <= 256, "loss: class count %d above 256", d);
+  GCNB_REQUIRE(ldh % 4 == 0 && ldg % 4 == 0 && (n_rows == 0 || (aligned16(h) && aligned16(g))),
+               "loss: row strides must be multiples of 4 floats and operands 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
-  const int grid = std::max(1, std::min((n_rows + WARPS - 1) / WARPS, LOSS_BLOCKS_MAX));
+  const int c4 = (d + 3) / 4;
+  int lpr = 1;
+  while (lpr < 32 && lpr < c4) lpr <<= 1;
+  const int vpl = (c4 + lpr - 1) / lpr;  // 1 or 2
+  const int rows_per_block = NT / lpr;
+  const int grid = std::max(1, std::min((n_rows + rows_per_block - 1) / rows_per_block, LOSS_BLOCKS_MAX));
   if (n_rows > 0) {
-    k_loss<<<grid, NT, 0, st>>>(h, ldh, n_rows, d, label, inv_n_labeled, g, ldg, act, scratch);
+    using LossFn = void (*)(const float4*, int, int, int, const int*, double, float4*, int, int, double*);
+    LossFn fn = vpl == 2 ? k_loss<32, 2>
+              : lpr == 1 ? k_loss<1, 1> : lpr == 2 ? k_loss<2, 1> : lpr == 4 ? k_loss<4, 1>
+              : lpr == 8 ? k_loss<8, 1> : lpr == 16 ? k_loss<16, 1> : k_loss<32, 1>;
+    fn<<<grid, NT, 0, st>>>(reinterpret_cast<const float4*>(h), ldh / 4, n_rows, d, label, inv_n_labeled,
+                            reinterpret_cast<float4*>(g), ldg / 4, act, scratch);
     GCNB_AFTER_LAUNCH("loss grad");
   }
   k_sum_partials_f64<<<1, 32, 0, st>>>(scratch, n_rows > 0 ? grid : 0, loss_sum);

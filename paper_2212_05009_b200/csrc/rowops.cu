@@ -4,6 +4,7 @@
 //   gcnb_fwd_layer_f32  runtime._fwd_compute       (runtime.py:297-306)
 //   gcnb_dense_f32      the `@ w` of runtime.py:299 hoisted before aggregation
 //   gcnb_bwd_layer_f32  runtime._bwd_compute       (runtime.py:344-356)
+//   gcnb_reduce_*       allreduce-side ΔW reduction (+ fused SGD, runtime.py:359-360)
 //
 // Design: the aggregation Σ_j A[r,j]·X[j] is HBM/L2-gather
 // bound.  A group of LPR lanes owns one CSR row; each lane owns a 16-byte
@@ -16,7 +17,6 @@
 // accumulation orders are fixed (CSR order per row, fixed tile→block map,
 // fixed partial-reduction order): reruns are bit-identical.
 #include <algorithm>
-#include <mutex>
 
 #include "common.cuh"
 
@@ -92,19 +92,19 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
 }
 
 // ---------------------------------------------------------------------------
-// Tile GEMM helper: acc[u] (rows trg + u*RG, cols 4tc..4tc+3) += Ys[r][k]·Ws[k][4tc..]
+// Tile GEMM: acc[u] (tile rows trg + u*RG, cols 4tc..4tc+3) = Σ_k Ys[r][k]·Ws[k][4tc..]
+template <int RPT>
 __device__ __forceinline__ void tile_gemm(const float* __restrict__ Ys, int ys_ld, const float* __restrict__ Ws,
-                                          int ws_ld, int K, int trg, int RG, int tc, int rpt,
-                                          float4 (&acc)[RPT_MAX]) {
+                                          int ws_ld, int K, int trg, int RG, int tc, int rpt, float4 (&acc)[RPT]) {
 #pragma unroll
-  for (int u = 0; u < RPT_MAX; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int u = 0; u < RPT; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4* W4 = reinterpret_cast<const float4*>(Ws);
   const int ws_ld4 = ws_ld / 4;
 #pragma unroll 4
   for (int k = 0; k < K; ++k) {
     const float4 w = W4[k * ws_ld4 + tc];
 #pragma unroll
-    for (int u = 0; u < RPT_MAX; ++u)
+    for (int u = 0; u < RPT; ++u)
       if (u < rpt) acc[u] = fma4(Ys[(trg + u * RG) * ys_ld + k], w, acc[u]);
   }
 }
@@ -155,7 +155,7 @@ __device__ __forceinline__ void stage_tile(const int* __restrict__ rp, const int
 
 // Forward layer with the dense transform fused: H[r] = act((A[r,:]·X)·W)
 // (AGG) or H[r] = act(X[r]·W) (!AGG, the hoisted dense transform).
-template <int LPR, int VPL, bool AGG>
+template <int LPR, int VPL, bool AGG, int RPT>
 __global__ void __launch_bounds__(NT) k_fwd_gemm(const int* __restrict__ rp, const int* __restrict__ col,
                                                  const float* __restrict__ val, const int* __restrict__ rows,
                                                  int n_rows, const float* __restrict__ X, int ldx, int d_in,
@@ -185,10 +185,10 @@ __global__ void __launch_bounds__(NT) k_fwd_gemm(const int* __restrict__ rp, con
                               c4i, Ys, ys_ld);
     __syncthreads();
     if (rpt > 0) {
-      float4 acc[RPT_MAX];
-      tile_gemm(Ys, ys_ld, Ws, ld_out, d_in, trg, RG, tc, rpt, acc);
+      float4 acc[RPT];
+      tile_gemm<RPT>(Ys, ys_ld, Ws, ld_out, d_in, trg, RG, tc, rpt, acc);
 #pragma unroll
-      for (int u = 0; u < RPT_MAX; ++u) {
+      for (int u = 0; u < RPT; ++u) {
         if (u < rpt) {
           const int i = t0 + trg + u * RG;
           if (i < n_rows) {
@@ -203,9 +203,9 @@ __global__ void __launch_bounds__(NT) k_fwd_gemm(const int* __restrict__ rp, con
 }
 
 // ---------------------------------------------------------------------------
-// Backward layer: agg = A_back[r,:]·G;  G_prev[r] = (agg·Wᵀ) ⊙ σ'(H_prev[r]);
+// Backward layer: agg = A_back[r,:]·G;  G_prev[r] = (agg·Wᵀ) ⊙ σ'(H_prev[r])  (GP);
 // per-block ΔW partial = Σ_r H_prev[r]ᵀ·agg[r]  (fixed tile order).
-template <int LPR, int VPL, int IPT_MAX>
+template <int LPR, int VPL, int IPT, bool GP, int RPT>
 __global__ void __launch_bounds__(NT) k_bwd(const int* __restrict__ rp, const int* __restrict__ col,
                                             const float* __restrict__ val, const int* __restrict__ rows,
                                             int n_rows, const float* __restrict__ G, int ldg, int d_k,
@@ -217,11 +217,10 @@ __global__ void __launch_bounds__(NT) k_bwd(const int* __restrict__ rp, const in
   const int ld_p = (d_prev + 3) & ~3;
   const int as_ld = ld_k + 4;
   const int hs_ld = ld_p + 4;
-  const bool with_gp = Gp != nullptr;
-  float* Wts = smem;                                  // d_k × ld_p  (Wᵀ), only with_gp
-  float* As = smem + (with_gp ? d_k * ld_p : 0);      // T × as_ld
-  float* Hs = As + T * as_ld;                         // T × hs_ld
-  if (with_gp) {
+  float* Wts = smem;                              // d_k × ld_p  (Wᵀ), GP only
+  float* As = smem + (GP ? d_k * ld_p : 0);       // T × as_ld
+  float* Hs = As + T * as_ld;                     // T × hs_ld
+  if (GP) {
     for (int idx = threadIdx.x; idx < d_k * ld_p; idx += NT) {
       const int c = idx / ld_p, i = idx - c * ld_p;
       Wts[idx] = i < d_prev ? __ldg(W + (size_t)i * ld_k + c) : 0.0f;
@@ -232,13 +231,22 @@ __global__ void __launch_bounds__(NT) k_bwd(const int* __restrict__ rp, const in
   const int RG = NT / c4p;
   const int tc = threadIdx.x % c4p, trg = threadIdx.x / c4p;
   const int rpt = trg < RG ? (T - trg + RG - 1) / RG : 0;
-  // ΔW mapping: rows i = ig + ii*RGi of ΔW (d_prev), cols 4kc.. (ld_k)
+  // ΔW mapping over the float4 chunks of the d_prev × ld_k partial (C chunks):
+  //  C >= NT: thread owns rows i = ig + ii*RGi, cols 4kc.., accumulating every tile row;
+  //  C <  NT: RS = NT / C row groups; thread owns one chunk for tile rows r ≡ rs (mod RS),
+  //           and the RS group partials are combined in a fixed order at the end.
+  const int C = d_prev * c4k;
+  const int RS = C >= NT ? 1 : NT / C;
+  const int CG = RS > 1 ? C : NT;
+  const int q = threadIdx.x % CG, rs = threadIdx.x / CG;
   const int RGi = NT / c4k;
-  const int kc = threadIdx.x % c4k, ig = threadIdx.x / c4k;
-  const int ipt = ig < RGi && ig < d_prev ? (d_prev - ig + RGi - 1) / RGi : 0;
-  float4 dw[IPT_MAX];
+  const int kc = q % c4k, ig = q / c4k;
+  int ipt;
+  if (RS > 1) ipt = rs < RS ? 1 : 0;
+  else ipt = ig < RGi && ig < d_prev ? (d_prev - ig + RGi - 1) / RGi : 0;
+  float4 dw[IPT];
 #pragma unroll
-  for (int ii = 0; ii < IPT_MAX; ++ii) dw[ii] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int ii = 0; ii < IPT; ++ii) dw[ii] = make_float4(0.f, 0.f, 0.f, 0.f);
 
   const int n_tiles = (n_rows + T - 1) / T;
   __syncthreads();
@@ -250,11 +258,11 @@ __global__ void __launch_bounds__(NT) k_bwd(const int* __restrict__ rp, const in
     stage_tile<LPR, VPL, false>(nullptr, nullptr, nullptr, rows, n_rows, t0, T,
                                 reinterpret_cast<const float4*>(Hp), ldhp / 4, c4p, Hs, hs_ld);
     __syncthreads();
-    if (with_gp && rpt > 0) {
-      float4 acc[RPT_MAX];
-      tile_gemm(As, as_ld, Wts, ld_p, d_k, trg, RG, tc, rpt, acc);
+    if (GP && rpt > 0) {
+      float4 acc[RPT];
+      tile_gemm<RPT>(As, as_ld, Wts, ld_p, d_k, trg, RG, tc, rpt, acc);
 #pragma unroll
-      for (int u = 0; u < RPT_MAX; ++u) {
+      for (int u = 0; u < RPT; ++u) {
         if (u < rpt) {
           const int r = trg + u * RG;
           const int i = t0 + r;
@@ -272,30 +280,83 @@ __global__ void __launch_bounds__(NT) k_bwd(const int* __restrict__ rp, const in
       }
     }
     if (ipt > 0) {
-      for (int r = 0; r < tv; ++r) {
+      for (int r = rs; r < tv; r += RS) {
         const float4 a = reinterpret_cast<const float4*>(As + r * as_ld)[kc];
         const float* hr = Hs + r * hs_ld + ig;
 #pragma unroll
-        for (int ii = 0; ii < IPT_MAX; ++ii)
+        for (int ii = 0; ii < IPT; ++ii)
           if (ii < ipt) dw[ii] = fma4(hr[ii * RGi], a, dw[ii]);
       }
     }
     __syncthreads();
   }
   float* part = partials + (size_t)blockIdx.x * d_prev * ld_k;
+  if (RS > 1) {
+    float4* red = reinterpret_cast<float4*>(Hs + T * hs_ld);  // NT float4 of dedicated scratch
+    if (ipt) red[rs * C + q] = dw[0];
+    __syncthreads();
+    if (threadIdx.x < C) {
+      float4 t = red[threadIdx.x];
+      for (int g = 1; g < RS; ++g) {
+        const float4 u = red[g * C + threadIdx.x];
+        t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+      }
+      reinterpret_cast<float4*>(part)[threadIdx.x] = t;  // chunk q == threadIdx.x
+    }
+    return;
+  }
 #pragma unroll
-  for (int ii = 0; ii < IPT_MAX; ++ii)
+  for (int ii = 0; ii < IPT; ++ii)
     if (ii < ipt) reinterpret_cast<float4*>(part + (size_t)(ig + ii * RGi) * ld_k)[kc] = dw[ii];
-  // rows of ΔW no thread owns (d_prev not covered) cannot exist: RGi*IPT >= d_prev by construction.
 }
 
-__global__ void k_reduce_partials(const float* __restrict__ partials, int n_slots, long long size,
-                                  float* __restrict__ out, int accumulate) {
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < size;
-       j += (long long)gridDim.x * blockDim.x) {
-    float s = accumulate ? out[j] : 0.0f;
-    for (int b = 0; b < n_slots; ++b) s += partials[(size_t)b * size + j];
-    out[j] = s;
+// out = Σ_s partials[s] in a fixed order (float4 chunks).  A 1024-thread block
+// owns 64 chunks; its 16 slot groups stride the slots with two independent
+// accumulators each and are combined in a fixed order.  With w != null the
+// SGD update w -= lr·out is fused (runtime.py:359-360).
+constexpr int RED_T = 1024;
+__global__ void __launch_bounds__(RED_T) k_reduce4(const float4* __restrict__ partials, int n_slots,
+                                                  long long size4, float4* __restrict__ out, int accumulate,
+                                                  float4* __restrict__ w, float lr) {
+  __shared__ float4 red[16][64];
+  const int lane = threadIdx.x & 63, grp = threadIdx.x >> 6;
+  const long long chunk = blockIdx.x * 64LL + lane;
+  // 8 independent accumulation chains per thread (slots grp + 16*(8*j + c)),
+  // combined in a fixed order: few dependent L2 round trips, deterministic.
+  constexpr int CH = 8;
+  float4 s[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (chunk < size4) {
+    for (int b0 = grp; b0 < n_slots; b0 += 16 * CH) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int b = b0 + 16 * c;
+        if (b < n_slots) {
+          const float4 u = __ldg(partials + (size_t)b * size4 + chunk);
+          s[c].x += u.x; s[c].y += u.y; s[c].z += u.z; s[c].w += u.w;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 1; c < CH; ++c) {
+    s[0].x += s[c].x; s[0].y += s[c].y; s[0].z += s[c].z; s[0].w += s[c].w;
+  }
+  red[grp][lane] = s[0];
+  __syncthreads();
+  if (grp == 0 && chunk < size4) {
+    float4 t = accumulate ? out[chunk] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int g = 0; g < 16; ++g) {
+      t.x += red[g][lane].x; t.y += red[g][lane].y; t.z += red[g][lane].z; t.w += red[g][lane].w;
+    }
+    out[chunk] = t;
+    if (w) {
+      float4 x = w[chunk];
+      x.x -= lr * t.x; x.y -= lr * t.y; x.z -= lr * t.z; x.w -= lr * t.w;
+      w[chunk] = x;
+    }
   }
 }
 
@@ -318,8 +379,6 @@ AggShape agg_shape(int d) {
 }
 
 int occupancy_grid(const void* fn, size_t smem, int n_tiles) {
-  int dev = 0;
-  cudaGetDevice(&dev);
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, smem) != cudaSuccess || per_sm < 1) {
@@ -329,60 +388,58 @@ int occupancy_grid(const void* fn, size_t smem, int n_tiles) {
   return std::max(1, std::min(n_tiles, per_sm * num_sms()));
 }
 
-// Tile height for an output width d_out (RPT_MAX rows per thread at most)
-// that is also a multiple of the aggregation group count NG.
-int tile_rows(int d_out, int lpr) {
+// Tile height for an output width d_out (<= RPT_MAX rows per thread) that is
+// also a multiple of the aggregation group count NG; *rpt_out = rows per thread.
+int tile_rows(int d_out, int lpr, int* rpt_out) {
   const int c4o = round4(d_out) / 4;
   const int rg = NT / c4o;
   const int ng = NT / lpr;
   int t = 4 * rg;
   t = ((t + ng - 1) / ng) * ng;
   while (t > RPT_MAX * rg && t > ng) t -= ng;
-  return std::max(t, ng);
+  t = std::max(t, ng);
+  *rpt_out = (t + rg - 1) / rg;
+  return t;
 }
+
+#define GCNB_LPR_CASES(M) M(2, 1) M(4, 1) M(8, 1) M(16, 1) M(32, 1) M(32, 2)
 
 using AggFn = void (*)(const int*, const int*, const float*, const int*, int, const float4*, int, int, float4*, int,
                        int);
 AggFn pick_agg(AggShape s) {
-  switch (s.lpr * 4 + s.vpl) {
-    case 2 * 4 + 1: return k_agg<2, 1>;
-    case 4 * 4 + 1: return k_agg<4, 1>;
-    case 8 * 4 + 1: return k_agg<8, 1>;
-    case 16 * 4 + 1: return k_agg<16, 1>;
-    case 32 * 4 + 1: return k_agg<32, 1>;
-    case 32 * 4 + 2: return k_agg<32, 2>;
-    default: return nullptr;
-  }
+#define M(L, V) if (s.lpr == L && s.vpl == V) return k_agg<L, V>;
+  GCNB_LPR_CASES(M)
+#undef M
+  return nullptr;
 }
 
 using FwdFn = void (*)(const int*, const int*, const float*, const int*, int, const float*, int, int, const float*,
                        int, float*, int, int, int);
+template <bool AGG, int RPT>
+FwdFn pick_fwd_rpt(AggShape s) {
+#define M(L, V) if (s.lpr == L && s.vpl == V) return k_fwd_gemm<L, V, AGG, RPT>;
+  GCNB_LPR_CASES(M)
+#undef M
+  return nullptr;
+}
 template <bool AGG>
-FwdFn pick_fwd(AggShape s) {
-  switch (s.lpr * 4 + s.vpl) {
-    case 2 * 4 + 1: return k_fwd_gemm<2, 1, AGG>;
-    case 4 * 4 + 1: return k_fwd_gemm<4, 1, AGG>;
-    case 8 * 4 + 1: return k_fwd_gemm<8, 1, AGG>;
-    case 16 * 4 + 1: return k_fwd_gemm<16, 1, AGG>;
-    case 32 * 4 + 1: return k_fwd_gemm<32, 1, AGG>;
-    case 32 * 4 + 2: return k_fwd_gemm<32, 2, AGG>;
-    default: return nullptr;
-  }
+FwdFn pick_fwd(AggShape s, int rpt) {
+  return rpt <= 4 ? pick_fwd_rpt<AGG, 4>(s) : pick_fwd_rpt<AGG, RPT_MAX>(s);
 }
 
 using BwdFn = void (*)(const int*, const int*, const float*, const int*, int, const float*, int, int, const float*,
                        int, int, const float*, float*, int, int, float*, int);
+template <int IPT, bool GP, int RPT>
+BwdFn pick_bwd_t(AggShape s) {
+#define M(L, V) if (s.lpr == L && s.vpl == V) return k_bwd<L, V, IPT, GP, RPT>;
+  GCNB_LPR_CASES(M)
+#undef M
+  return nullptr;
+}
 template <int IPT>
-BwdFn pick_bwd_ipt(AggShape s) {
-  switch (s.lpr * 4 + s.vpl) {
-    case 2 * 4 + 1: return k_bwd<2, 1, IPT>;
-    case 4 * 4 + 1: return k_bwd<4, 1, IPT>;
-    case 8 * 4 + 1: return k_bwd<8, 1, IPT>;
-    case 16 * 4 + 1: return k_bwd<16, 1, IPT>;
-    case 32 * 4 + 1: return k_bwd<32, 1, IPT>;
-    case 32 * 4 + 2: return k_bwd<32, 2, IPT>;
-    default: return nullptr;
-  }
+BwdFn pick_bwd_ipt(AggShape s, bool gp, int rpt) {
+  if (gp) return rpt <= 4 ? pick_bwd_t<IPT, true, 4>(s) : pick_bwd_t<IPT, true, RPT_MAX>(s);
+  return pick_bwd_t<IPT, false, 4>(s);  // no S-GEMM without G_prev: RPT is unused
 }
 
 struct BwdPlan {
@@ -397,15 +454,17 @@ int bwd_plan(int n_rows, int d_prev, int d_k, bool with_gp, BwdPlan* out) {
   const int ld_k = round4(d_k), ld_p = round4(d_prev);
   const int c4k = ld_k / 4;
   const int rgi = NT / c4k;
-  const int ipt = (d_prev + rgi - 1) / rgi;
+  const int ipt = d_prev * c4k < NT ? 1 : (d_prev + rgi - 1) / rgi;
+  int rpt = 0;
+  const int T = tile_rows(d_prev, s.lpr, &rpt);
   BwdFn fn = nullptr;
-  if (ipt <= 4) fn = pick_bwd_ipt<4>(s);
-  else if (ipt <= 16) fn = pick_bwd_ipt<16>(s);
-  else if (ipt <= 32) fn = pick_bwd_ipt<32>(s);
+  if (ipt <= 1) fn = pick_bwd_ipt<1>(s, with_gp, rpt);
+  else if (ipt <= 4) fn = pick_bwd_ipt<4>(s, with_gp, rpt);
+  else if (ipt <= 16) fn = pick_bwd_ipt<16>(s, with_gp, rpt);
+  else if (ipt <= 32) fn = pick_bwd_ipt<32>(s, with_gp, rpt);
   GCNB_REQUIRE(fn != nullptr, "bwd layer: unsupported widths d_prev=%d d_k=%d", d_prev, d_k);
-  const int T = tile_rows(d_prev, s.lpr);
-  const size_t smem =
-      sizeof(float) * ((with_gp ? (size_t)d_k * ld_p : 0) + (size_t)T * (ld_k + 4) + (size_t)T * (ld_p + 4));
+  const size_t smem = sizeof(float) * ((with_gp ? (size_t)d_k * ld_p : 0) + (size_t)T * (ld_k + 4) +
+                                       (size_t)T * (ld_p + 4) + 4 * NT);
   GCNB_REQUIRE(smem <= 227 * 1024, "bwd layer: tile does not fit shared memory (d_prev=%d d_k=%d)", d_prev, d_k);
   const int n_tiles = std::max(1, (n_rows + T - 1) / T);
   out->fn = fn;
@@ -418,6 +477,22 @@ int bwd_plan(int n_rows, int d_prev, int d_k, bool with_gp, BwdPlan* out) {
 int check_csr_args(const int32_t* row_ptr, const int32_t* col, const float* val, int32_t n_rows) {
   GCNB_REQUIRE(n_rows >= 0, "n_rows must be >= 0");
   GCNB_REQUIRE(n_rows == 0 || (row_ptr && col && val), "CSR arrays must be non-null");
+  return GCNB_OK;
+}
+
+int launch_fwd_gemm(bool agg, const int32_t* row_ptr, const int32_t* col, const float* val, const int32_t* rows,
+                    int32_t n_rows, const float* x, int32_t ldx, int32_t d_in, const float* w, int32_t d_out,
+                    float* h, int32_t ldh, int32_t act, cudaStream_t st, const char* what) {
+  const AggShape s = agg_shape(d_in);
+  int rpt = 0;
+  const int T = tile_rows(d_out, s.lpr, &rpt);
+  FwdFn fn = agg ? pick_fwd<true>(s, rpt) : pick_fwd<false>(s, rpt);
+  GCNB_REQUIRE(fn != nullptr, "%s: unsupported width %d", what, d_in);
+  const size_t smem = sizeof(float) * ((size_t)d_in * round4(d_out) + (size_t)T * (round4(d_in) + 4));
+  GCNB_REQUIRE(smem <= 227 * 1024, "%s: tile does not fit shared memory", what);
+  const int grid = occupancy_grid(reinterpret_cast<const void*>(fn), smem, (n_rows + T - 1) / T);
+  fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, x, ldx, d_in, w, d_out, h, ldh, act, T);
+  GCNB_AFTER_LAUNCH(what);
   return GCNB_OK;
 }
 
@@ -457,9 +532,9 @@ extern "C" int gcnb_fwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
                "fwd layer: row strides must be multiples of 4 and cover the widths");
   GCNB_REQUIRE(aligned16(x) && aligned16(h) && (!w || aligned16(w)), "fwd layer: operands must be 16-byte aligned");
   if (n_rows == 0) return GCNB_OK;
-  const AggShape s = agg_shape(d_in);
   cudaStream_t st = (cudaStream_t)stream;
   if (!w) {
+    const AggShape s = agg_shape(d_in);
     AggFn fn = pick_agg(s);
     const int rows_per_block = NT / s.lpr;
     const int grid = std::max(1, std::min((n_rows + rows_per_block - 1) / rows_per_block, num_sms() * 8));
@@ -468,14 +543,8 @@ extern "C" int gcnb_fwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
     GCNB_AFTER_LAUNCH("fwd layer (aggregate)");
     return GCNB_OK;
   }
-  FwdFn fn = pick_fwd<true>(s);
-  const int T = tile_rows(d_out, s.lpr);
-  const size_t smem = sizeof(float) * ((size_t)d_in * round4(d_out) + (size_t)T * (round4(d_in) + 4));
-  GCNB_REQUIRE(smem <= 227 * 1024, "fwd layer: tile does not fit shared memory");
-  const int grid = occupancy_grid(reinterpret_cast<const void*>(fn), smem, (n_rows + T - 1) / T);
-  fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, x, ldx, d_in, w, d_out, h, ldh, act, T);
-  GCNB_AFTER_LAUNCH("fwd layer (aggregate+transform)");
-  return GCNB_OK;
+  return launch_fwd_gemm(true, row_ptr, col, val, rows, n_rows, x, ldx, d_in, w, d_out, h, ldh, act, st,
+                         "fwd layer (aggregate+transform)");
 }
 
 extern "C" int gcnb_dense_f32(const float* x, int32_t ldx, int32_t n_rows, int32_t d_in, const float* w,
@@ -486,16 +555,8 @@ extern "C" int gcnb_dense_f32(const float* x, int32_t ldx, int32_t n_rows, int32
                "dense: row strides must be multiples of 4 and cover the widths");
   GCNB_REQUIRE(x && w && y && aligned16(x) && aligned16(w) && aligned16(y), "dense: operands must be 16-byte aligned");
   if (n_rows == 0) return GCNB_OK;
-  const AggShape s = agg_shape(d_in);
-  FwdFn fn = pick_fwd<false>(s);
-  const int T = tile_rows(d_out, s.lpr);
-  const size_t smem = sizeof(float) * ((size_t)d_in * round4(d_out) + (size_t)T * (round4(d_in) + 4));
-  GCNB_REQUIRE(smem <= 227 * 1024, "dense: tile does not fit shared memory");
-  const int grid = occupancy_grid(reinterpret_cast<const void*>(fn), smem, (n_rows + T - 1) / T);
-  fn<<<grid, NT, smem, (cudaStream_t)stream>>>(nullptr, nullptr, nullptr, nullptr, n_rows, x, ldx, d_in, w, d_out,
-                                               y, ldy, GCNB_ACT_IDENTITY, T);
-  GCNB_AFTER_LAUNCH("dense");
-  return GCNB_OK;
+  return launch_fwd_gemm(false, nullptr, nullptr, nullptr, nullptr, n_rows, x, ldx, d_in, w, d_out, y, ldy,
+                         GCNB_ACT_IDENTITY, (cudaStream_t)stream, "dense");
 }
 
 extern "C" int gcnb_bwd_grid(int32_t n_rows, int32_t d_prev, int32_t d_k, int32_t with_gprev, int32_t* grid_out) {
@@ -529,13 +590,24 @@ extern "C" int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
   return GCNB_OK;
 }
 
+extern "C" int gcnb_reduce_sgd_f32(const float* partials, int32_t n_slots, int64_t size, float* out,
+                                   int32_t accumulate, float* w, float lr, void* stream) {
+  GCNB_REQUIRE(n_slots >= 0 && size >= 0 && size % 4 == 0, "reduce partials: size must be a multiple of 4");
+  GCNB_REQUIRE(out && (n_slots == 0 || partials), "reduce partials: null operands");
+  GCNB_REQUIRE(aligned16(out) && (!partials || aligned16(partials)) && (!w || aligned16(w)),
+               "reduce partials: operands must be 16-byte aligned");
+  GCNB_REQUIRE(!w || (lr > 0.0f && lr < 1e30f), "reduce+sgd: learning rate must be positive and finite");
+  if (size == 0) return GCNB_OK;
+  const long long size4 = size / 4;
+  const int grid = (int)((size4 + 63) / 64);
+  k_reduce4<<<grid, RED_T, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4*>(partials), n_slots, size4,
+                                                      reinterpret_cast<float4*>(out), accumulate,
+                                                      reinterpret_cast<float4*>(w), lr);
+  GCNB_AFTER_LAUNCH(w ? "reduce partials + sgd" : "reduce partials");
+  return GCNB_OK;
+}
+
 extern "C" int gcnb_reduce_partials_f32(const float* partials, int32_t n_slots, int64_t size, float* out,
                                         int32_t accumulate, void* stream) {
-  GCNB_REQUIRE(n_slots >= 0 && size >= 0, "reduce partials: negative sizes");
-  GCNB_REQUIRE(out && (n_slots == 0 || partials), "reduce partials: null operands");
-  if (size == 0) return GCNB_OK;
-  const int grid = (int)std::min<int64_t>((size + NT - 1) / NT, num_sms() * 4);
-  k_reduce_partials<<<grid, NT, 0, (cudaStream_t)stream>>>(partials, n_slots, size, out, accumulate);
-  GCNB_AFTER_LAUNCH("reduce partials");
-  return GCNB_OK;
+  return gcnb_reduce_sgd_f32(partials, n_slots, size, out, accumulate, nullptr, 0.0f, stream);
 }

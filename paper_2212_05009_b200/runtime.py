@@ -418,11 +418,13 @@ class ProcState:
                       0 if gp is None else gp.shape[1], self.act, part.data_ptr(), self.stream())
         return used
 
-    def reduce_dw(self, k: int, n_slots: int) -> None:
+    def reduce_dw(self, k: int, n_slots: int, apply_sgd: bool = False) -> None:
+        """ΔW^k = Σ of the layer's block partials (fixed order); optionally fused with SGD."""
         size = self.dw[k].numel()
-        with span(f"reduce{k}", 4 * size * (n_slots + 1), size * n_slots, self.stream()):
-            _lib.call("gcnb_reduce_partials_f32", self.partials[k].data_ptr(), n_slots, size,
-                      self.dw[k].data_ptr(), 0, self.stream())
+        algo = 4 * size * (n_slots + 1) + (8 * size if apply_sgd else 0)
+        with span(f"reduce{k}", algo, size * n_slots, self.stream()):
+            _lib.call("gcnb_reduce_sgd_f32", self.partials[k].data_ptr(), n_slots, size, self.dw[k].data_ptr(), 0,
+                      self.w[k].data_ptr() if apply_sgd else None, float(self.learning_rate), self.stream())
 
     def sgd(self, k: int, dw: torch.Tensor) -> None:
         size = self.w[k].numel()
@@ -539,16 +541,21 @@ def _backward(states, net, n_labeled: int, epoch: int, step: int, loss_out: torc
         for st in states:
             st.pack_to("bwd", k, bases)
         _log_phase(states, net, "bwd", k, epoch, step)
+        if len(states) == 1:
+            # one rank: the ΔW reduction and the SGD step are one kernel
+            st = states[0]
+            used = st.bwd_compute(k, "all")
+            st.reduce_dw(k, used, apply_sgd=True)
+            st.dw_total[k] = st.dw[k]
+            continue
         for st in states:
             used = st.bwd_compute(k, "all")
             st.reduce_dw(k, used)
-    # allreduce_sum of every layer's ΔW in ascending rank order, then SGD on every replica
-    for k in range(1, L + 1):
-        total = states[0].dw[k]
-        if len(states) > 1:
-            total = states[0].dw_sum[k]
-            _lib.call("gcnb_sum_buffers_f32", _lib.ptr_array([st.dw[k].data_ptr() for st in states]), len(states),
-                      total.numel(), total.data_ptr(), states[0].stream())
+        # allreduce_sum of ΔW^k in ascending rank order, then SGD on every replica.
+        # Updating W^k right after its layer is exact: no later (lower) layer reads W^k.
+        total = states[0].dw_sum[k]
+        _lib.call("gcnb_sum_buffers_f32", _lib.ptr_array([st.dw[k].data_ptr() for st in states]), len(states),
+                  total.numel(), total.data_ptr(), states[0].stream())
         for st in states:
             st.dw_total[k] = total
             st.sgd(k, total)
