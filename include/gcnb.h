@@ -173,6 +173,18 @@ int gcnb_sum_buffers_f32(const float* const* bufs, int32_t p, int64_t n,
 int gcnb_sum_buffers_f64(const double* const* bufs, int32_t p, int64_t n,
                          double* out, void* stream);
 
+/* Distributed allreduce_sum over NVLink (runtime.py:147-157, 127-133):
+ * gcnb_push_f32 copies src (n floats, n % 4 == 0) into n_dst destinations
+ * (each rank's slot inside every peer's slot buffer, peer-mapped) and rings
+ * *flags[i] (+1, system-scope release) after all stores are visible;
+ * gcnb_wait_flags on the receiver then gcnb_sum_slots_f32 sums the p slots
+ * in ascending rank order: out[j] = Σ_r slots[r*stride + j] (j < n_f32), and
+ * *loss_out = Σ_r (double at slots + r*stride + n_f32) when loss_out != NULL. */
+int gcnb_push_f32(const float* src, int64_t n, float* const* dst, uint64_t* const* flags,
+                  int32_t n_dst, int32_t* counter, void* stream);
+int gcnb_sum_slots_f32(const float* slots, int32_t p, int64_t stride, int64_t n_f32,
+                       float* out, double* loss_out, void* stream);
+
 /* runtime._apply_update (runtime.py:359-360): W -= lr·ΔW (n floats). */
 int gcnb_sgd_f32(float* w, const float* dw, int64_t n, float lr, void* stream);
 

@@ -195,6 +195,50 @@ __global__ void k_sum_partials_f64(const double* __restrict__ partials, int n, d
   if (threadIdx.x == 0) *out = t;
 }
 
+// One vector pushed to several (peer) destinations, then one doorbell per
+// destination once every block's stores are visible (the allreduce_sum
+// contribution exchange of runtime.py:147-157 over NVLink).
+struct PushArgs {
+  float4* dst[GCNB_MAX_PEERS];
+  unsigned long long* flag[GCNB_MAX_PEERS];
+  int n_dst;
+};
+
+__global__ void __launch_bounds__(NT) k_push(const float4* __restrict__ src, long long n4, PushArgs a, int* counter) {
+  const long long work = n4 * a.n_dst;
+  for (long long t = blockIdx.x * (long long)NT + threadIdx.x; t < work; t += (long long)gridDim.x * NT) {
+    const int d = (int)(t / n4);
+    const long long j = t - (long long)d * n4;
+    a.dst[d][j] = __ldg(src + j);
+  }
+  __threadfence_system();
+  __syncthreads();
+  __shared__ int last;
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence_system();
+    *counter = 0;
+    for (int d = 0; d < a.n_dst; ++d) red_release_sys_add(a.flag[d], 1ull);
+  }
+}
+
+// out[j] = Σ_r slots[r*stride + j] in ascending rank order; the f64 in the two
+// words after n_f32 of every slot is summed the same way into *loss.
+__global__ void k_sum_slots(const float* __restrict__ slots, int p, long long stride, long long n_f32,
+                            float* __restrict__ out, double* loss) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n_f32; j += (long long)gridDim.x * blockDim.x) {
+    float s = slots[j];
+    for (int r = 1; r < p; ++r) s += slots[(size_t)r * stride + j];
+    out[j] = s;
+  }
+  if (loss && blockIdx.x == 0 && threadIdx.x == 0) {
+    double t = 0.0;
+    for (int r = 0; r < p; ++r) t += *reinterpret_cast<const double*>(slots + (size_t)r * stride + n_f32);
+    *loss = t;
+  }
+}
+
 struct PtrArgsF {
   const float* p[GCNB_MAX_PEERS];
 };
@@ -322,6 +366,36 @@ extern "C" int gcnb_loss_grad_f32(const float* h, int32_t ldh, int32_t n_rows, i
   }
   k_sum_partials_f64<<<1, 32, 0, st>>>(scratch, n_rows > 0 ? grid : 0, loss_sum);
   GCNB_AFTER_LAUNCH("loss sum");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_push_f32(const float* src, int64_t n, float* const* dst, uint64_t* const* flags, int32_t n_dst,
+                             int32_t* counter, void* stream) {
+  GCNB_REQUIRE(n_dst >= 1 && n_dst <= GCNB_MAX_PEERS, "push: n_dst=%d out of range", n_dst);
+  GCNB_REQUIRE(n > 0 && n % 4 == 0, "push: length must be a positive multiple of 4");
+  GCNB_REQUIRE(src && dst && flags && counter && aligned16(src), "push: null or misaligned arguments");
+  PushArgs a{};
+  a.n_dst = n_dst;
+  for (int d = 0; d < n_dst; ++d) {
+    GCNB_REQUIRE(dst[d] && aligned16(dst[d]) && flags[d], "push: destination %d invalid", d);
+    a.dst[d] = reinterpret_cast<float4*>(dst[d]);
+    a.flag[d] = reinterpret_cast<unsigned long long*>(flags[d]);
+  }
+  const long long work = (n / 4) * n_dst;
+  const int grid = (int)std::max<long long>(1, std::min<long long>((work + NT - 1) / NT, num_sms() * 2));
+  k_push<<<grid, NT, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4*>(src), n / 4, a, counter);
+  GCNB_AFTER_LAUNCH("push");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_sum_slots_f32(const float* slots, int32_t p, int64_t stride, int64_t n_f32, float* out,
+                                  double* loss_out, void* stream) {
+  GCNB_REQUIRE(p >= 1 && n_f32 >= 0 && stride >= n_f32 + (loss_out ? 2 : 0), "sum slots: bad shapes");
+  GCNB_REQUIRE(slots && out, "sum slots: null operands");
+  GCNB_REQUIRE(!loss_out || ((n_f32 % 2) == 0 && (stride % 2) == 0), "sum slots: loss words must be 8-byte aligned");
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n_f32 + NT - 1) / NT, num_sms() * 4));
+  k_sum_slots<<<grid, NT, 0, (cudaStream_t)stream>>>(slots, p, stride, n_f32, out, loss_out);
+  GCNB_AFTER_LAUNCH("sum slots");
   return GCNB_OK;
 }
 

@@ -1,0 +1,474 @@
+"""One process per GPU: the halo exchange and ΔW allreduce over NVLink peer memory.
+
+This is the B200 realisation of the reference's threads scheduler
+(runtime.py:391-440: one worker per rank, blocking receives, barrier-backed
+allreduce) with `SimNetwork` (runtime.py:67-144) replaced by direct NVLink
+stores:
+
+* every rank allocates one device *arena* (cudaMalloc) holding the buffers
+  peers write into — the [own | halo] operand blocks of every layer/phase,
+  the allreduce slots and the doorbell counters — and publishes its CUDA IPC
+  handle plus buffer offsets through torch.distributed (rendezvous only);
+* a send (`_fwd_send`/`_bwd_send`, runtime.py:289-294, 336-341) is one pack
+  kernel that gathers the plan rows and stores them straight into each
+  receiver's halo slot, then rings a per-(src,dst) doorbell (system-scope
+  release increment) — `gcnb_pack_rows_f32`;
+* a receive (runtime.py:300-304, 347-351) is `gcnb_wait_flags` (acquire,
+  with a timeout that surfaces as CommError), issued AFTER the interior-row
+  kernel so the transfer overlaps the interior SpMM;
+* the allreduce (runtime.py:147-157) pushes the rank's packed
+  [ΔW^1..ΔW^L | loss] vector into every rank's slot, waits for the p-1
+  doorbells and sums the slots in ascending rank order — identical on every
+  rank, as the reference's rank-ordered sum.  Slots are double-buffered by
+  epoch parity (two captured CUDA graphs), which together with the
+  per-epoch allreduce makes buffer reuse race-free.
+
+Host-side schedule/layout logic (`RankSchedule`, `arena_layout`) is
+device-free so it is covered by the gloo world-size-2 tests on CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+import time
+
+import numpy as np
+
+from . import _lib
+from .comm import build_comm_plan
+from .layout import build_rank_layout
+from .sparse import transpose_sparse
+
+ALIGN = 256
+
+
+# ---------------------------------------------------------------------------
+# host-only pieces (CPU-testable)
+
+
+def widths(dims, transform_first):
+    """(forward operand width, backward width) per layer k = 1..L."""
+    L = len(dims) - 1
+    fw = [None] + [dims[k] if transform_first[k] else dims[k - 1] for k in range(1, L + 1)]
+    bw = [None] + [dims[k] for k in range(1, L + 1)]
+    return fw, bw
+
+
+def ld_of(d: int) -> int:
+    return (int(d) + 3) // 4 * 4
+
+
+def arena_layout(n_own: int, r_fwd: int, r_bwd: int, dims, transform_first, p: int, n_pack: int) -> dict:
+    """Byte offsets of every peer-visible buffer inside one rank's arena."""
+    L = len(dims) - 1
+    fw, bw = widths(dims, transform_first)
+    off, cur = {}, 0
+
+    def take(name, nbytes):
+        nonlocal cur
+        off[name] = cur
+        cur += (int(nbytes) + ALIGN - 1) // ALIGN * ALIGN
+
+    for k in range(1, L + 1):
+        take(f"xext{k}", (n_own + r_fwd) * ld_of(fw[k]) * 4)
+        take(f"gext{k}", (n_own + r_bwd) * ld_of(bw[k]) * 4)
+    slot = n_pack + 4
+    take("slots", 2 * p * slot * 4)
+    take("flags_halo", 8 * p)
+    take("flags_ar", 8 * p)
+    take("expected_halo", 8 * p)
+    take("expected_ar", 8 * p)
+    take("counter", 16)
+    take("err", 16)
+    off["_total"] = cur
+    off["_slot"] = slot
+    return off
+
+
+class RankSchedule:
+    """Who sends to / waits for whom in every exchange of an epoch."""
+
+    def __init__(self, plan_fwd, plan_bwd, rank: int, n_layers: int):
+        self.rank = rank
+        self.p = plan_fwd.p
+        self.L = n_layers
+        self.fwd_dst = [n for n in range(self.p) if n != rank and len(plan_fwd.send[rank][n])]
+        self.fwd_src = [int(s) for s in plan_fwd.recv_from[rank]]
+        self.bwd_dst = [n for n in range(self.p) if n != rank and len(plan_bwd.send[rank][n])]
+        self.bwd_src = [int(s) for s in plan_bwd.recv_from[rank]]
+
+    def exchanges(self):
+        """[(phase, layer, dsts, srcs)] in epoch order (fwd k=1..L, bwd k=L..1)."""
+        out = [("fwd", k, self.fwd_dst, self.fwd_src) for k in range(1, self.L + 1)]
+        out += [("bwd", k, self.bwd_dst, self.bwd_src) for k in range(self.L, 0, -1)]
+        return out
+
+    def doorbells_rung(self):
+        """(dst, count) of halo doorbells this rank rings per epoch."""
+        cnt = {}
+        for _, _, dsts, _ in self.exchanges():
+            for d in dsts:
+                cnt[d] = cnt.get(d, 0) + 1
+        return cnt
+
+    def doorbells_awaited(self):
+        cnt = {}
+        for _, _, _, srcs in self.exchanges():
+            for s in srcs:
+                cnt[s] = cnt.get(s, 0) + 1
+        return cnt
+
+
+def build_rank(a_hat, owner, p: int, rank: int, directed: bool):
+    """Global plans + this rank's layout (every rank computes the same plans)."""
+    plan_fwd = build_comm_plan(a_hat, owner, p)
+    if directed:
+        a_bwd = transpose_sparse(a_hat)
+        plan_bwd = build_comm_plan(a_bwd, owner, p)
+    else:
+        a_bwd, plan_bwd = a_hat, plan_fwd
+    layout = build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, rank)
+    return plan_fwd, plan_bwd, layout
+
+
+def halo_bytes_per_epoch(layout, dims, transform_first) -> int:
+    """Bytes this rank stores into peers per epoch (fwd + bwd exchanges)."""
+    fw, bw = widths(dims, transform_first)
+    L = len(dims) - 1
+    rf = int(layout.fwd.send_ptr[-1]) if len(layout.fwd.send_ptr) else 0
+    rb = int(layout.bwd.send_ptr[-1]) if len(layout.bwd.send_ptr) else 0
+    return sum(4 * ld_of(fw[k]) * rf + 4 * ld_of(bw[k]) * rb for k in range(1, L + 1))
+
+
+def reference_words_per_epoch(layout, dims) -> int:
+    """The reference's accounting: rows × d_{k-1} forward, rows × d_k backward (runtime.py:51-64)."""
+    L = len(dims) - 1
+    rf = int(layout.fwd.send_ptr[-1]) if len(layout.fwd.send_ptr) else 0
+    rb = int(layout.bwd.send_ptr[-1]) if len(layout.bwd.send_ptr) else 0
+    return sum(rf * dims[k - 1] + rb * dims[k] for k in range(1, L + 1))
+
+
+# ---------------------------------------------------------------------------
+# device side
+
+
+class _CAI:
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class Arena:
+    """One cudaMalloc'd, IPC-exportable block carved into torch views."""
+
+    def __init__(self, offsets: dict, device):
+        import torch
+
+        self.off = offsets
+        self.device = device
+        ptr = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _lib.call("gcnb_malloc", ctypes.byref(ptr), offsets["_total"])
+            self.base = ptr.value
+            _lib.call("gcnb_memset_async", self.base, 0, offsets["_total"], None)
+            torch.cuda.synchronize(device)
+
+    def tensor(self, name: str, shape, dtype):
+        import torch
+
+        typestr = {torch.float32: "<f4", torch.float64: "<f8", torch.int64: "<i8", torch.int32: "<i4"}[dtype]
+        with torch.cuda.device(self.device):
+            return torch.as_tensor(_CAI(self.base + self.off[name], shape, typestr), device=self.device)
+
+    def rows_alloc(self, name: str, rows: int, width: int):
+        import torch
+
+        return self.tensor(name, (rows, ld_of(width)), torch.float32)
+
+    def handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _lib.call("gcnb_ipc_get_handle", self.base, buf)
+        return buf.raw
+
+    def free(self):
+        if self.base:
+            _lib.call("gcnb_free", self.base)
+            self.base = 0
+
+
+class DistributedTrainer:
+    """Full-batch training of this process's rank; collective over torch.distributed."""
+
+    def __init__(self, a_hat, h0, owner, p: int, model, labels, directed: bool, device, timeout_ms: int = 20000):
+        import torch
+        import torch.distributed as dist
+
+        from .runtime import ProcState
+
+        self.rank = dist.get_rank()
+        self.p = p
+        self.device = device
+        self.timeout_ms = timeout_ms
+        plan_fwd, plan_bwd, layout = build_rank(a_hat, owner, p, self.rank, directed)
+        self.layout = layout
+        self.sched = RankSchedule(plan_fwd, plan_bwd, self.rank, len(model.dims) - 1)
+        dims = tuple(int(d) for d in model.dims)
+        L = len(dims) - 1
+        tf = [False] + [dims[k] < dims[k - 1] for k in range(1, L + 1)]
+        sizes = [dims[k - 1] * ld_of(dims[k]) for k in range(1, L + 1)]
+        n_pack = int(sum(sizes))
+        n_own = len(layout.global_rows)
+        self.off = arena_layout(n_own, layout.fwd.n_halo, layout.bwd.n_halo, dims, tf, p, n_pack)
+        torch.cuda.set_device(device)
+        self.arena = Arena(self.off, device)
+        self.st = ProcState(layout, plan_fwd, plan_bwd, model, np.asarray(h0)[layout.global_rows], device,
+                            alloc=self.arena.rows_alloc)
+        assert self.st.transform_first == tf and self.st.n_pack == n_pack
+        self.n_lab = len(labels)
+        self.st.set_labels(labels)
+        a = self.arena
+        self.flags_halo = a.tensor("flags_halo", (p,), torch.int64)
+        self.flags_ar = a.tensor("flags_ar", (p,), torch.int64)
+        self.expected_halo = a.tensor("expected_halo", (p,), torch.int64)
+        self.expected_ar = a.tensor("expected_ar", (p,), torch.int64)
+        self.counter = a.tensor("counter", (4,), torch.int32)
+        self.err = a.tensor("err", (4,), torch.int32)
+        self.slot = self.off["_slot"]
+        self.slots = a.tensor("slots", (2, p, self.slot), torch.float32)
+        self.loss_total = torch.zeros(1, dtype=torch.float64, device=device)
+        # rendezvous: handles + offsets + own-row counts
+        info = {"handle": a.handle(), "off": self.off, "n_own": n_own, "rank": self.rank}
+        infos = [None] * p
+        dist.all_gather_object(infos, info)
+        self.peer_base = {}
+        for r, inf in enumerate(infos):
+            if r == self.rank:
+                self.peer_base[r] = a.base
+                continue
+            ptr = ctypes.c_void_p()
+            _lib.call("gcnb_ipc_open_handle", inf["handle"], ctypes.byref(ptr))
+            self.peer_base[r] = ptr.value
+        self.infos = infos
+        self.fwd_bases = [None] + [{r: (self.peer_base[r] + infos[r]["off"][f"xext{k}"], infos[r]["n_own"])
+                                    for r in range(p)} for k in range(1, L + 1)]
+        self.bwd_bases = [None] + [{r: (self.peer_base[r] + infos[r]["off"][f"gext{k}"], infos[r]["n_own"])
+                                    for r in range(p)} for k in range(1, L + 1)]
+        me = self.rank
+        self.halo_flag_fwd = [self.peer_base[d] + infos[d]["off"]["flags_halo"] + 8 * me for d in layout.fwd.send_dst]
+        self.halo_flag_bwd = [self.peer_base[d] + infos[d]["off"]["flags_halo"] + 8 * me for d in layout.bwd.send_dst]
+        self.ar_dst = [[self.peer_base[r] + infos[r]["off"]["slots"] + 4 * (q * p * self.slot + me * self.slot)
+                        for r in range(p)] for q in (0, 1)]
+        self.ar_flag = [self.peer_base[r] + infos[r]["off"]["flags_ar"] + 8 * me for r in range(p)]
+        self.ar_srcs = [r for r in range(p) if r != me]
+        torch.cuda.synchronize(device)
+        dist.barrier()
+        self.graphs = {}
+
+    # -- one epoch ------------------------------------------------------------
+    def _wait(self, flags, expected, srcs):
+        if not srcs:
+            return
+        _lib.call("gcnb_wait_flags", flags.data_ptr(), _lib.int_array(srcs), len(srcs), expected.data_ptr(),
+                  self.err.data_ptr(), self.timeout_ms, self.st.stream())
+
+    def enqueue_epoch(self, parity: int, comm: bool = True) -> None:
+        st, L = self.st, self.st.n_layers
+        cnt = self.counter.data_ptr()
+        for k in range(1, L + 1):
+            st.fwd_transform(k)
+            if comm:
+                st.pack_to("fwd", k, self.fwd_bases[k], flags=self.halo_flag_fwd, counter=cnt)
+            st.fwd_compute(k, "interior")
+            if comm:
+                self._wait(self.flags_halo, self.expected_halo, self.sched.fwd_src)
+            st.fwd_compute(k, "boundary")
+        st.loss_grad(1.0 / self.n_lab)
+        for k in range(L, 0, -1):
+            if comm:
+                st.pack_to("bwd", k, self.bwd_bases[k], flags=self.halo_flag_bwd, counter=cnt)
+            gi = st.bwd_compute(k, "interior", slot=0)
+            if comm:
+                self._wait(self.flags_halo, self.expected_halo, self.sched.bwd_src)
+            gb = st.bwd_compute(k, "boundary", slot=gi)
+            st.reduce_dw(k, gi + gb)
+        n_tot = st.n_pack + 4
+        from .profiling import span
+
+        if comm:
+            with span("allreduce_push", 4 * n_tot * self.p, 0, st.stream()):
+                _lib.call("gcnb_push_f32", st.dwpack.data_ptr(), n_tot, _lib.ptr_array(self.ar_dst[parity]),
+                          _lib.ptr_array(self.ar_flag), self.p, cnt, st.stream())
+            self._wait(self.flags_ar, self.expected_ar, self.ar_srcs)
+            slots = self.slots[parity]
+            _lib.call("gcnb_sum_slots_f32", slots.data_ptr(), self.p, self.slot, st.n_pack, st.dwsum_pack.data_ptr(),
+                      self.loss_total.data_ptr(), st.stream())
+        else:
+            _lib.call("gcnb_sum_slots_f32", st.dwpack.data_ptr(), 1, self.slot, st.n_pack, st.dwsum_pack.data_ptr(),
+                      self.loss_total.data_ptr(), st.stream())
+        with span("sgd", 12 * st.n_pack, 2 * st.n_pack, st.stream()):
+            _lib.call("gcnb_sgd_f32", st.wpack.data_ptr(), st.dwsum_pack.data_ptr(), st.n_pack,
+                      float(st.learning_rate), st.stream())
+        for k in range(1, L + 1):
+            st.dw_total[k] = st.dw_sum[k]
+        st._has_trace = st._has_grad = True
+
+    def capture(self, key, parity: int, comm: bool = True, timer=None) -> None:
+        import torch
+
+        from . import profiling
+
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with profiling.active(timer):
+            with torch.cuda.graph(g, capture_error_mode="relaxed"):
+                self.enqueue_epoch(parity, comm)
+        self.graphs[key] = g
+
+    def check(self) -> None:
+        if int(self.err[0].item()) != 0:
+            raise _lib.CommError(f"rank {self.rank}: a halo/allreduce doorbell timed out "
+                                 f"(after {self.timeout_ms} ms)")
+
+    def close(self) -> None:
+        for r, base in self.peer_base.items():
+            if r != self.rank:
+                _lib.call("gcnb_ipc_close_handle", base)
+        self.peer_base = {}
+
+
+# ---------------------------------------------------------------------------
+# bench entry (launched by torchrun, one process per GPU)
+
+
+def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summary, cpu_epoch_timer, METRIC, UNIT):
+    import torch
+    import torch.distributed as dist
+
+    from . import profiling
+    from .host import PartitionConfig, random_partition
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun --nproc-per-node {args.gpus}")
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    dist.init_process_group(backend="cpu:gloo,cuda:nccl", device_id=device)
+    wl = build_workload(args.workload, args.seed)
+    n = wl["n"]
+    t0 = time.perf_counter()
+    if args.partition == "hp":
+        from .hp import partition_hypergraph
+
+        pi = partition_hypergraph(wl["a_hat"], world, seed=args.seed)
+    else:
+        pi = random_partition(wl["a_hat"].row_nnz(), PartitionConfig(p=world, seed=args.seed, epsilon=0.01))
+    t_part = time.perf_counter() - t0
+    tr = DistributedTrainer(wl["a_hat"], wl["h0"], pi.assignment, world, wl["model"], wl["labels"], wl["directed"],
+                            device)
+    st = tr.st
+    from . import _lib as L_
+
+    c0 = L_.launch_count()
+    tr.enqueue_epoch(0)
+    torch.cuda.synchronize()
+    launches = L_.launch_count() - c0
+    tr.check()
+    for i in range(1, max(args.warmup, 3)):
+        tr.enqueue_epoch(i % 2)
+    torch.cuda.synchronize()
+    tr.check()
+    # the next timed epoch index must continue the parity sequence
+    start_parity = max(args.warmup, 3) % 2
+    timers = {0: profiling.KernelTimer(), 1: profiling.KernelTimer()}
+    tr.capture(0, 0, True, timers[0])
+    tr.capture(1, 1, True, timers[1])
+    tr.capture("compute", 0, False, None)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    rows = []
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            q = (start_parity + i) % 2
+            flush.zero_()
+            evs[i][0].record()
+            tr.graphs[q].replay()
+            evs[i][1].record()
+            evs[i][1].synchronize()
+            rows.extend(timers[q].results())
+    torch.cuda.synchronize()
+    dist.barrier()
+    tr.check()
+    ms_rank = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    # compute-only epochs (no sends, waits or allreduce) for the exposed-communication share
+    cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        cev[i][0].record()
+        tr.graphs["compute"].replay()
+        cev[i][1].record()
+        cev[i][1].synchronize()
+    ms_compute = float(np.mean([a.elapsed_time(b) for a, b in cev]))
+    # end to end: own features H2D from pinned memory, one eager epoch, loss D2H
+    d0 = wl["dims"][0]
+    h0_pinned = torch.from_numpy(np.asarray(wl["h0"][tr.layout.global_rows], dtype=np.float32)).pin_memory()
+    e2e = []
+    par = (start_parity + args.steps) % 2
+    dist.barrier()
+    for i in range(0 if args.kernels_only else max(3, min(args.steps, 20))):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        st.hbuf[0][:, :d0].copy_(h0_pinned, non_blocking=True)
+        tr.enqueue_epoch(par)
+        loss = float(tr.loss_total.item()) / len(wl["labels"])
+        e2e.append(time.perf_counter() - t)
+        par ^= 1
+    tr.check()
+    e2e_ms = 1e3 * float(np.mean(e2e)) if e2e else float("nan")
+    vals = torch.tensor([ms_rank, ms_compute, e2e_ms], dtype=torch.float64, device=device)
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    halo = torch.tensor([halo_bytes_per_epoch(tr.layout, st.dims, st.transform_first),
+                         reference_words_per_epoch(tr.layout, st.dims)], dtype=torch.float64, device=device)
+    dist.all_reduce(halo, op=dist.ReduceOp.SUM)
+    peak, peak_kind = measured_peaks()
+    compute_rows = [r for r in rows if not r[0].startswith(("pack", "allreduce"))]
+    kname, achieved, kms, kbytes, table = roofline_summary(compute_rows, peak, peak_kind, args.steps)
+    pack = [r for r in rows if r[0].startswith("pack")]
+    nvl = None
+    if pack:
+        sent = sum(4 * 0 + r[1] for r in pack)  # algorithmic pack bytes (read + write)
+        t_ms = sum(r[3] for r in pack)
+        nvl = round(sent / 2 / (t_ms * 1e-3) / 1e9, 1) if t_ms > 0 else None
+    clk = clocks.summary()
+    ms, msc, e2e_max = (float(x) for x in vals.tolist())
+    line = {
+        "metric": METRIC, "value": round(ms, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl["name"], "n": n, "nnz_ahat": wl["nnz"], "dims": list(wl["dims"]),
+                   "directed": wl["directed"], "partition": args.partition, "partition_s": round(t_part, 2),
+                   "l2": "flushed (512 MiB write) before every step", "graph": True, "seed": args.seed,
+                   "transport": "NVLink peer stores + doorbells (CUDA IPC), P2P allreduce"},
+        "e2e": {"value": round(e2e_max, 4), "unit": UNIT,
+                "h2d_bytes_per_step": int(h0_pinned.numel() * 4), "d2h_bytes_per_step": 8},
+        "gpu_launches": int(launches * args.steps),
+        "roofline": {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "algo_bytes_per_launch": kbytes, "ms_per_launch": round(kms, 5)},
+        "kernels": table,
+        "halo_bytes_per_epoch": int(halo[0].item()), "reference_words_per_epoch": int(halo[1].item()),
+        "exposed_comm_pct": round(100.0 * max(0.0, ms - msc) / ms, 2), "compute_only_ms": round(msc, 4),
+        "nvlink_pack_gbs_rank0": nvl,
+        "cpu_baseline": None,
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    tr.close()
+    dist.destroy_process_group()

@@ -207,7 +207,13 @@ class ProcState:
     access.  `weights` supports item assignment (uploads that replica only).
     """
 
-    def __init__(self, layout: RankLayout, plan_fwd: CommPlan, plan_bwd: CommPlan, model, h0: np.ndarray, dev):
+    def __init__(self, layout: RankLayout, plan_fwd: CommPlan, plan_bwd: CommPlan, model, h0: np.ndarray, dev,
+                 alloc=None):
+        """`alloc(name, rows, width)` places the peer-written [own | halo] blocks
+        (default: private device memory; distributed.py passes an IPC arena)."""
+        if alloc is None:
+            def alloc(name, rows, width):
+                return devmem.empty_rows(rows, width, dev)
         self.rank = layout.rank
         self.global_rows = layout.global_rows
         self.plan_fwd = plan_fwd
@@ -235,19 +241,31 @@ class ProcState:
             self.hbuf = [None] * (L + 1)   # H^k own rows
             for k in range(1, L + 1):
                 width = self.dims[k] if self.transform_first[k] else self.dims[k - 1]
-                self.xext[k] = devmem.empty_rows(n + R_f, width, dev)
+                self.xext[k] = alloc(f"xext{k}", n + R_f, width)
             for k in range(0, L + 1):
                 if k < L and not self.transform_first[k + 1]:
                     self.hbuf[k] = self.xext[k + 1][:n]
                 else:
                     self.hbuf[k] = devmem.empty_rows(n, self.dims[k], dev)
             self.hbuf[0][:, : self.dims[0]].copy_(torch.from_numpy(np.asarray(h0, dtype=np.float32)))
-            self.gext = [None] + [devmem.empty_rows(n + R_b, self.dims[k], dev) for k in range(1, L + 1)]
-            self.w = [None] + [devmem.empty_rows(self.dims[k - 1], self.dims[k], dev) for k in range(1, L + 1)]
+            self.gext = [None] + [alloc(f"gext{k}", n + R_b, self.dims[k]) for k in range(1, L + 1)]
+            # W^1..W^L and ΔW^1..ΔW^L each live in one packed vector, so the ΔW
+            # allreduce and the SGD step are single launches; 4 tail floats carry
+            # the rank's f64 loss sum through the distributed allreduce.
+            sizes = [self.dims[k - 1] * devmem.ld_of(self.dims[k]) for k in range(1, L + 1)]
+            self.pack_offsets = [0] + list(np.cumsum(sizes).tolist())
+            self.n_pack = int(self.pack_offsets[-1])
+
+            def views(buf):
+                return [None] + [buf[o:o + s].view(self.dims[k - 1], -1) for k, o, s in
+                                 zip(range(1, L + 1), self.pack_offsets[:-1], sizes)]
+
+            self.wpack = torch.zeros(self.n_pack + 4, dtype=torch.float32, device=dev)
+            self.dwpack = torch.zeros(self.n_pack + 4, dtype=torch.float32, device=dev)
+            self.dwsum_pack = torch.zeros(self.n_pack + 4, dtype=torch.float32, device=dev)
+            self.w, self.dw, self.dw_sum = views(self.wpack), views(self.dwpack), views(self.dwsum_pack)
             for k in range(1, L + 1):
                 self._upload_weight(k - 1, model.weights[k - 1])
-            self.dw = [None] + [torch.zeros_like(self.w[k]) for k in range(1, L + 1)]
-            self.dw_sum = [None] + [torch.zeros_like(self.w[k]) for k in range(1, L + 1)]
             self.dw_total = [None] * (L + 1)  # allreduced ΔW of the last backward sweep
             # ΔW partial slots: interior launch + boundary launch (or one all-rows launch)
             self.bwd_grids = [None] * (L + 1)
@@ -263,7 +281,8 @@ class ProcState:
                                                dtype=torch.float32, device=dev)
             self.label = torch.full((max(n, 1),), -1, dtype=torch.int32, device=dev)
             self.loss_scratch = torch.zeros(_lib.loss_scratch_doubles(), dtype=torch.float64, device=dev)
-            self.loss_sum = torch.zeros(1, dtype=torch.float64, device=dev)
+            # the rank's NLL sum lives in the ΔW pack tail (it travels with the allreduce)
+            self.loss_sum = self.dwpack[self.n_pack:self.n_pack + 2].view(torch.float64)
 
     # -- reference-compatible host views ---------------------------------
     @property
