@@ -1,0 +1,196 @@
+"""Hypergraph (HP) partitioning: recursive bisection with connectivity-1 FM.
+
+Restates the reference partitioner (gcnpart partition.py:486-559,
+`partition_hypergraph_fm` / `_partition_by_bisection` / `_recursive_bisect`)
+with the per-bisection engine in C++ (csrc_host/partition.cpp, bucketed
+gains) instead of O(n)-per-move Python.  The recursion, the rng stream
+([seed, 0x4850]: one draw per restart, left subtree before right), the
+per-side caps and the final k-way repair stay here, in the same order as the
+reference, so small instances give the reference's assignment bit-exactly
+(tests/test_hp.py pins this against gcnpart's own output).
+
+The column-net model of Â (net j = rows with a nonzero in column j, unit
+cost, vertex weight = row nnz; models.py:175-186) is built as the pattern of
+Âᵀ; directed inputs are partitioned on the symmetrised pattern as the
+reference's CLI does (cli.py:162-176, 225).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+from .host import BalanceInfeasibleError, Partition, PartitionConfig, _weight_repair
+
+PKG = Path(__file__).resolve().parent
+HOST_LIB = PKG / "lib" / "libgcnb_host.so"
+HOST_SRC = PKG / "csrc_host" / "partition.cpp"
+_hlib = None
+
+
+def build_host(force: bool = False) -> Path:
+    if force or not HOST_LIB.exists() or HOST_SRC.stat().st_mtime > HOST_LIB.stat().st_mtime:
+        HOST_LIB.parent.mkdir(exist_ok=True)
+        cxx = "/usr/bin/g++" if Path("/usr/bin/g++").exists() else "g++"
+        tmp = HOST_LIB.with_suffix(".so.tmp")
+        subprocess.run([cxx, "-O3", "-std=c++17", "-fPIC", "-shared", "-o", str(tmp), str(HOST_SRC)], check=True)
+        os.replace(tmp, HOST_LIB)
+    return HOST_LIB
+
+
+def _load():
+    global _hlib
+    if _hlib is None:
+        if not HOST_LIB.exists():
+            raise ImportError(f"{HOST_LIB} missing: run __graft_entry__.build()")
+        lib = ctypes.CDLL(str(HOST_LIB))
+        vp, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+        lib.gcnb_hp_bisect.argtypes = [i32, i32, vp, vp, vp, vp, f64, i64, vp, i32, i32, i32, vp, vp]
+        lib.gcnb_hp_bisect.restype = ctypes.c_int
+        _hlib = lib
+    return _hlib
+
+
+class NetList:
+    """Hypergraph as CSR over nets: pins of net j = pins[ptr[j]:ptr[j+1]] (ascending)."""
+
+    def __init__(self, n_vertices: int, ptr: np.ndarray, pins: np.ndarray, cost=None, vertex_weight=None):
+        self.n = int(n_vertices)
+        self.ptr = np.ascontiguousarray(ptr, dtype=np.int64)
+        self.pins = np.ascontiguousarray(pins, dtype=np.int64)
+        m = len(self.ptr) - 1
+        self.cost = np.ones(m, dtype=np.int64) if cost is None else np.asarray(cost, dtype=np.int64)
+        self.vertex_weight = (np.ones(self.n, dtype=np.int64) if vertex_weight is None
+                              else np.asarray(vertex_weight, dtype=np.int64))
+
+    @property
+    def n_nets(self) -> int:
+        return len(self.ptr) - 1
+
+    @classmethod
+    def from_hypergraph(cls, h) -> "NetList":
+        """From a gcnpart-style Hypergraph (`nets` list of pin arrays)."""
+        lens = np.array([len(p) for p in h.nets], dtype=np.int64)
+        ptr = np.concatenate([[0], np.cumsum(lens)])
+        pins = np.concatenate([np.asarray(p, dtype=np.int64) for p in h.nets]) if len(h.nets) else np.zeros(0, int)
+        return cls(h.n_vertices, ptr, pins, h.net_cost, h.vertex_weight)
+
+    def restrict(self, ids: np.ndarray):
+        """Nets restricted to the sorted vertex subset `ids`, keeping nets with
+        >= 2 remaining pins, pins renumbered to positions in ids (partition.py:546-555)."""
+        pos = np.full(self.n, -1, dtype=np.int64)
+        pos[ids] = np.arange(len(ids))
+        local = pos[self.pins]
+        keep = local >= 0
+        net_of = np.repeat(np.arange(self.n_nets), np.diff(self.ptr))
+        cnt = np.bincount(net_of[keep], minlength=self.n_nets)
+        good = cnt >= 2
+        sel = keep & good[net_of]
+        new_ptr = np.concatenate([[0], np.cumsum(cnt[good])]).astype(np.int64)
+        return new_ptr, local[sel].astype(np.int32), self.cost[good].astype(np.int32)
+
+
+def column_net_model(a) -> NetList:
+    """models.py:175-186: net j pins the rows with a nonzero in column j."""
+    if a.n_rows != a.n_cols:
+        raise ValueError("matrix must be square")
+    ro = np.asarray(a.row_offsets, dtype=np.int64)
+    ci = np.asarray(a.col_indices, dtype=np.int64)
+    rows = np.repeat(np.arange(a.n_rows, dtype=np.int64), np.diff(ro))
+    order = np.argsort(ci, kind="stable")
+    ptr = np.zeros(a.n_cols + 1, dtype=np.int64)
+    np.cumsum(np.bincount(ci, minlength=a.n_cols), out=ptr[1:])
+    diag = np.zeros(a.n_rows, dtype=bool)
+    diag[rows[rows == ci]] = True
+    if not diag.all():
+        raise ValueError("column-net model requires a full diagonal (self loops)")
+    return NetList(a.n_rows, ptr, rows[order], None, np.diff(ro))
+
+
+def symmetrized(a):
+    """Union pattern of A and Aᵀ with unit values (cli.py:162-176)."""
+    from .sparse import CsrMatrix
+
+    ro = np.asarray(a.row_offsets, dtype=np.int64)
+    ci = np.asarray(a.col_indices, dtype=np.int64)
+    rows = np.repeat(np.arange(a.n_rows, dtype=np.int64), np.diff(ro))
+    n = a.n_rows
+    keys = np.unique(np.concatenate([rows * n + ci, ci * n + rows]))
+    r, c = keys // n, keys % n
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=n), out=rp[1:])
+    return CsrMatrix(n, n, rp, c, np.ones(len(c)))
+
+
+def _bisect_node(h: NetList, ids: np.ndarray, weights: np.ndarray, cap: float, min_count: int, seeds, cfg):
+    ptr, pins, cost = h.restrict(ids)
+    w = np.ascontiguousarray(weights[ids].astype(np.float64))
+    side = np.empty(len(ids), dtype=np.int8)
+    seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int32))
+    cut = ctypes.c_int64(0)
+    rc = _load().gcnb_hp_bisect(len(ids), len(ptr) - 1, ptr.ctypes.data, pins.ctypes.data, cost.ctypes.data,
+                                w.ctypes.data, float(cap), int(min_count), seeds.ctypes.data, len(seeds),
+                                int(cfg.fm_passes), int(bool(cfg.refinement)), side.ctypes.data, ctypes.byref(cut))
+    if rc != 0:
+        raise ValueError("hp bisection: invalid input")
+    return side
+
+
+def _recursive_bisect(h, ids, p_sub, part_base, assignment, weights, cap_leaf, rng, cfg):
+    if p_sub == 1:
+        assignment[ids] = part_base
+        return
+    if len(ids) < p_sub:
+        raise BalanceInfeasibleError("fewer vertices than parts in a bisection")
+    cap = (p_sub // 2) * cap_leaf
+    min_count = p_sub // 2
+    seeds = [int(rng.integers(0, len(ids))) for _ in range(cfg.restarts)]
+    side = _bisect_node(h, ids, weights, cap, min_count, seeds, cfg)
+    _recursive_bisect(h, ids[side == 0], p_sub // 2, part_base, assignment, weights, cap_leaf, rng, cfg)
+    _recursive_bisect(h, ids[side == 1], p_sub // 2, part_base + p_sub // 2, assignment, weights, cap_leaf, rng, cfg)
+
+
+def partition_hypergraph_fm(h, cfg: PartitionConfig) -> Partition:
+    """HP on a hypergraph (NetList or gcnpart Hypergraph) — partition.py:544-559."""
+    if not isinstance(h, NetList):
+        h = NetList.from_hypergraph(h)
+    n = h.n
+    weights = np.asarray(h.vertex_weight, dtype=np.int64)
+    if cfg.p > n:
+        raise ValueError(f"p={cfg.p} exceeds vertex count {n}")
+    if cfg.p == 1:
+        return Partition.from_assignment(np.zeros(n, dtype=np.int64), weights, 1, cfg.epsilon)
+    if cfg.p & (cfg.p - 1):
+        raise ValueError(f"internal partitioners use recursive bisection and need p to be a power of two "
+                         f"(got {cfg.p}); use an external partition file for other p")
+    cap_leaf = (1.0 + cfg.epsilon) * float(weights.sum()) / cfg.p
+    rng = np.random.default_rng([int(cfg.seed), 0x4850])
+    assignment = np.full(n, -1, dtype=np.int64)
+    _recursive_bisect(h, np.arange(n, dtype=np.int64), cfg.p, 0, assignment, weights, cap_leaf, rng, cfg)
+    pi = Partition.from_assignment(assignment, weights, cfg.p, cfg.epsilon)
+    if not pi.is_balanced():
+        assignment = _weight_repair(assignment, weights, cfg.p, cfg.epsilon)
+        pi = Partition.from_assignment(assignment, weights, cfg.p, cfg.epsilon)
+        if not pi.is_balanced():
+            raise BalanceInfeasibleError("partition violates the balance constraint")
+    return pi
+
+
+def partition_hypergraph(a_hat, p: int, seed: int = 0, epsilon: float = 0.01, directed: bool | None = None,
+                         fm_passes: int = 8, restarts: int = 3) -> Partition:
+    """HP of a normalised adjacency: column-net model of Â (of its symmetrised
+    pattern for directed inputs)."""
+    if directed is None:
+        ro = np.asarray(a_hat.row_offsets)
+        ci = np.asarray(a_hat.col_indices)
+        from .sparse import transpose_sparse
+
+        t = transpose_sparse(a_hat)
+        directed = not (np.array_equal(ro, t.row_offsets) and np.array_equal(ci, t.col_indices))
+    model = symmetrized(a_hat) if directed else a_hat
+    cfg = PartitionConfig(p=p, epsilon=epsilon, seed=seed, fm_passes=fm_passes, restarts=restarts)
+    return partition_hypergraph_fm(column_net_model(model), cfg)

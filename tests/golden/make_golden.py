@@ -193,8 +193,34 @@ def kat(g, helpers):
     np.savez_compressed(OUT / "kat.npz", **out)
 
 
+def partitions(g, helpers):
+    """HP assignments of gcnpart's own partition_hypergraph_fm (partition.py:544-559)
+    on small seeded instances (the sizes its O(n)-per-move FM finishes quickly)."""
+    out = {}
+    cases = [(40, 0.1, 1, 2, 0.05), (60, 0.08, 2, 4, 0.05), (120, 0.04, 3, 8, 0.05), (300, 0.02, 4, 4, 0.03),
+             (500, 0.01, 5, 8, 0.05)]
+    for i, (n, dens, seed, p, eps) in enumerate(cases):
+        raw = helpers.random_undirected(n, dens, seed)
+        a = g.normalize_adjacency(raw)
+        pi = g.partition_hypergraph_fm(g.build_hypergraph_model(a), g.PartitionConfig(p=p, seed=seed, epsilon=eps))
+        out[f"c{i}_case"] = np.array([n, p, seed], dtype=np.float64)
+        out[f"c{i}_dens_eps"] = np.array([dens, eps])
+        out[f"c{i}_assign"] = pi.assignment
+        out[f"c{i}_cut"] = np.float64(g.evaluate_hypergraph_cut(g.build_hypergraph_model(a), pi).cut_value)
+    # directed instance partitioned on the symmetrised pattern, as the CLI does
+    raw = helpers.random_directed(200, 0.02, 9)
+    a = g.normalize_adjacency(raw)
+    from gcnpart import cli
+
+    pi = g.partition_hypergraph_fm(g.build_hypergraph_model(cli._symmetrized(a)),
+                                   g.PartitionConfig(p=4, seed=9, epsilon=0.05))
+    out["dir_assign"] = pi.assignment
+    np.savez_compressed(OUT / "partitions.npz", **out)
+
+
 def main():
     g, helpers = _import_reference()
+    partitions(g, helpers)
     kat(g, helpers)
     small_instances(g, helpers)
     minibatch(g, helpers)

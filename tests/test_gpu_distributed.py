@@ -1,0 +1,30 @@
+"""Multi-GPU parity of the NVLink path: runs scripts/dist_check.py under torchrun
+on every visible GPU (>= 2) and requires the fp64 oracle's loss and weights
+within 1e-4 and bit-identical replicas.  Skipped on single-GPU boxes."""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.mark.parametrize("extra", [[], ["--directed"], ["--directed", "--graph", "--epochs", "4"]])
+def test_torchrun_parity(extra):
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + len(extra)), str(ROOT / "scripts" / "dist_check.py"),
+           *extra]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, "OMP_NUM_THREADS": "1"})
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    rep = json.loads(lines[-1])
+    assert rep["ok"] and rep["replicas_identical"]

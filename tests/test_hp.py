@@ -1,0 +1,63 @@
+"""Hypergraph partitioner (HP): bit-exact with the reference's own assignments
+on small instances (tests/golden/partitions.npz, written by running gcnpart's
+partition_hypergraph_fm), plus model/validation checks.  CPU only."""
+
+import numpy as np
+import pytest
+
+import paper_2212_05009_b200 as gb
+from oracle import gcn_oracle as o
+from paper_2212_05009_b200 import hp
+from tests.golden_data import load
+
+hp.build_host()
+
+
+def _a_hat(raw):
+    return gb.normalize_adjacency(gb.CsrMatrix(raw.n_rows, raw.n_cols, raw.row_offsets, raw.col_indices, raw.values))
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_hp_matches_reference_assignment(i):
+    z = load("partitions")
+    n, p, seed = (int(x) for x in z[f"c{i}_case"])
+    dens, eps = z[f"c{i}_dens_eps"]
+    a = _a_hat(o.random_undirected(n, float(dens), seed))
+    pi = hp.partition_hypergraph_fm(hp.column_net_model(a), gb.PartitionConfig(p=p, seed=seed, epsilon=float(eps)))
+    assert np.array_equal(pi.assignment, z[f"c{i}_assign"])
+    assert pi.is_balanced()
+
+
+def test_hp_directed_uses_symmetrised_model():
+    z = load("partitions")
+    a = _a_hat(o.random_directed(200, 0.02, 9))
+    pi = hp.partition_hypergraph(a, 4, seed=9, epsilon=0.05)
+    assert np.array_equal(pi.assignment, z["dir_assign"])
+
+
+def test_hp_cut_equals_plan_volume_and_beats_rp():
+    # locality graph: a 30x30 grid, randomly relabelled
+    side = 30
+    n = side * side
+    v = np.arange(n).reshape(side, side)
+    e = np.concatenate([np.stack([v[:, :-1].ravel(), v[:, 1:].ravel()], 1), np.stack([v[:-1].ravel(), v[1:].ravel()], 1)])
+    perm = np.random.default_rng(0).permutation(n)
+    r, c = perm[e[:, 0]], perm[e[:, 1]]
+    a = gb.normalize_adjacency(gb.CsrMatrix.from_coo(n, n, np.concatenate([r, c]), np.concatenate([c, r])))
+    pi = hp.partition_hypergraph(a, 4, seed=1)
+    plan = gb.build_comm_plan(a, pi)
+    h = hp.column_net_model(a)
+    lam = np.array([len(np.unique(pi.assignment[h.pins[h.ptr[j]:h.ptr[j + 1]]])) for j in range(h.n_nets)])
+    assert gb.plan_volume(plan, 1).total_words == int((lam - 1).sum())  # cut = volume (comm.py / PAPER Thm)
+    rp = gb.random_partition(a.row_nnz(), gb.PartitionConfig(p=4, seed=1))
+    assert gb.plan_volume(plan, 1).total_words < 0.3 * gb.plan_volume(gb.build_comm_plan(a, rp), 1).total_words
+
+
+def test_hp_validation():
+    a = _a_hat(o.random_undirected(30, 0.2, 1))
+    with pytest.raises(ValueError):
+        hp.partition_hypergraph(a, 3)
+    with pytest.raises(ValueError):
+        hp.column_net_model(gb.CsrMatrix.from_coo(3, 3, [0], [1]))
+    pi = hp.partition_hypergraph(a, 1)
+    assert np.all(pi.assignment == 0)
