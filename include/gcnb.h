@@ -144,7 +144,8 @@ int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* 
                        float* dw_partials, void* stream);
 
 /* out[j] = (accumulate ? out[j] : 0) + Σ_{s < n_slots} partials[s*size + j],
- * summed in slot order (fixed), j < size. */
+ * summed in a fixed (deterministic) order, j < size, size % 4 == 0.  The
+ * partials buffer is scratch: it is folded in place when n_slots > 64. */
 int gcnb_reduce_partials_f32(const float* partials, int32_t n_slots, int64_t size,
                              float* out, int32_t accumulate, void* stream);
 /* The same reduction with the SGD step of runtime._apply_update
@@ -184,6 +185,10 @@ int gcnb_push_f32(const float* src, int64_t n, float* const* dst, uint64_t* cons
                   int32_t n_dst, int32_t* counter, void* stream);
 int gcnb_sum_slots_f32(const float* slots, int32_t p, int64_t stride, int64_t n_f32,
                        float* out, double* loss_out, void* stream);
+/* Ring n doorbells (+1, system-scope release) after all prior stores of the
+ * stream's earlier kernels: with gcnb_wait_flags this is a device-side barrier
+ * across processes (the barrier of SimNetwork.allreduce, runtime.py:127-133). */
+int gcnb_signal_peers(uint64_t* const* flags, int32_t n, void* stream);
 
 /* runtime._apply_update (runtime.py:359-360): W -= lr·ΔW (n floats). */
 int gcnb_sgd_f32(float* w, const float* dw, int64_t n, float lr, void* stream);

@@ -63,6 +63,7 @@ _SIGNATURES = {
     "gcnb_sgd_f32": (_c_int, [_vp, _vp, _c_i64, _f32, _vp]),
     "gcnb_push_f32": (_c_int, [_vp, _c_i64, _vp, _vp, _c_int, _vp, _vp]),
     "gcnb_sum_slots_f32": (_c_int, [_vp, _c_int, _c_i64, _c_i64, _vp, _vp, _vp]),
+    "gcnb_signal_peers": (_c_int, [_vp, _c_int, _vp]),
     "gcnb_cast_pad_f64_f32": (_c_int, [_vp, _c_int, _c_i64, _c_int, _vp, _c_int, _vp]),
 }
 

@@ -388,6 +388,27 @@ extern "C" int gcnb_push_f32(const float* src, int64_t n, float* const* dst, uin
   return GCNB_OK;
 }
 
+__global__ void k_signal(PushArgs a) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int d = 0; d < a.n_dst; ++d) red_release_sys_add(a.flag[d], 1ull);
+  }
+}
+
+extern "C" int gcnb_signal_peers(uint64_t* const* flags, int32_t n, void* stream) {
+  GCNB_REQUIRE(n >= 0 && n <= GCNB_MAX_PEERS && (n == 0 || flags), "signal: bad arguments");
+  if (n == 0) return GCNB_OK;
+  PushArgs a{};
+  a.n_dst = n;
+  for (int d = 0; d < n; ++d) {
+    GCNB_REQUIRE(flags[d] != nullptr, "signal: null flag %d", d);
+    a.flag[d] = reinterpret_cast<unsigned long long*>(flags[d]);
+  }
+  k_signal<<<1, 32, 0, (cudaStream_t)stream>>>(a);
+  GCNB_AFTER_LAUNCH("signal peers");
+  return GCNB_OK;
+}
+
 extern "C" int gcnb_sum_slots_f32(const float* slots, int32_t p, int64_t stride, int64_t n_f32, float* out,
                                   double* loss_out, void* stream) {
   GCNB_REQUIRE(p >= 1 && n_f32 >= 0 && stride >= n_f32 + (loss_out ? 2 : 0), "sum slots: bad shapes");

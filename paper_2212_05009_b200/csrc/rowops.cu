@@ -22,26 +22,39 @@
 
 namespace gcnb {
 
-// Cooperative aggregation of one CSR row by a group of LPR lanes.  Must be
-// called by all 32 lanes of the warp (warp-uniform trip count); row < 0
-// marks an idle group.
-template <int LPR, int VPL>
-__device__ __forceinline__ void aggregate_row(const int* __restrict__ rp, const int* __restrict__ col,
-                                              const float* __restrict__ val, int row,
-                                              const float4* __restrict__ X4, int ldx4, int c4, int gl,
-                                              float4 (&acc)[VPL]) {
-  int s = 0, len = 0;
+// Row extent [s, s+len) of CSR row `row` (row < 0: empty).
+__device__ __forceinline__ void row_extent(const int* __restrict__ rp, int row, int& s, int& len) {
+  s = 0;
+  len = 0;
   if (row >= 0) {
     s = __ldg(rp + row);
     len = __ldg(rp + row + 1) - s;
   }
+}
+
+// Cooperative aggregation of one CSR row (extent s, len) by a group of LPR
+// lanes.  Must be called by all 32 lanes of the warp (warp-uniform trip
+// count).  The (col, val) chunk for the next LPR nonzeros is loaded before
+// the current chunk's gathers are issued, so the index stream and the
+// feature-row gathers overlap instead of forming two dependent round trips
+// per chunk.
+template <int LPR, int VPL>
+__device__ __forceinline__ void aggregate_span(const int* __restrict__ col, const float* __restrict__ val, int s,
+                                               int len, const float4* __restrict__ X4, int ldx4, int c4, int gl,
+                                               float4 (&acc)[VPL]) {
   const int maxlen = __reduce_max_sync(0xffffffffu, len);
+  int cj = 0;
+  float vj = 0.0f;
+  if (gl < len) {
+    cj = __ldg(col + s + gl);
+    vj = __ldg(val + s + gl);
+  }
   for (int base = 0; base < maxlen; base += LPR) {
-    int cj = 0;
-    float vj = 0.0f;
-    if (base + gl < len) {
-      cj = __ldg(col + s + base + gl);
-      vj = __ldg(val + s + base + gl);
+    int cn = 0;
+    float vn = 0.0f;
+    if (base + LPR + gl < len) {
+      cn = __ldg(col + s + base + LPR + gl);
+      vn = __ldg(val + s + base + LPR + gl);
     }
     const int cnt = min(LPR, maxlen - base);
 #pragma unroll 8
@@ -57,7 +70,19 @@ __device__ __forceinline__ void aggregate_row(const int* __restrict__ rp, const 
         }
       }
     }
+    cj = cn;
+    vj = vn;
   }
+}
+
+template <int LPR, int VPL>
+__device__ __forceinline__ void aggregate_row(const int* __restrict__ rp, const int* __restrict__ col,
+                                              const float* __restrict__ val, int row,
+                                              const float4* __restrict__ X4, int ldx4, int c4, int gl,
+                                              float4 (&acc)[VPL]) {
+  int s, len;
+  row_extent(rp, row, s, len);
+  aggregate_span<LPR, VPL>(col, val, s, len, X4, ldx4, c4, gl, acc);
 }
 
 // ---------------------------------------------------------------------------
@@ -73,14 +98,20 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
   const int gw = lane / LPR;
   const int warp_global = (blockIdx.x * NT + threadIdx.x) >> 5;
   const int n_warps = gridDim.x * WARPS;
-  for (int i0 = warp_global * GPW; i0 < n_rows; i0 += n_warps * GPW) {
-    const int i = i0 + gw;
-    int row = -1;
-    if (i < n_rows) row = rows ? __ldg(rows + i) : i;
+  const int stride = n_warps * GPW;
+  auto row_of = [&](int i) { return i < n_rows ? (rows ? __ldg(rows + i) : i) : -1; };
+  int row = row_of(warp_global * GPW + gw);
+  int s, len;
+  row_extent(rp, row, s, len);
+  for (int i0 = warp_global * GPW; i0 < n_rows; i0 += stride) {
+    // prefetch the next row's extent while this row is aggregated
+    const int row_n = row_of(i0 + stride + gw);
+    int s_n, len_n;
+    row_extent(rp, row_n, s_n, len_n);
     float4 acc[VPL];
 #pragma unroll
     for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    aggregate_row<LPR, VPL>(rp, col, val, row, X4, ldx4, c4, gl, acc);
+    aggregate_span<LPR, VPL>(col, val, s, len, X4, ldx4, c4, gl, acc);
     if (row >= 0) {
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
@@ -88,6 +119,9 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
         if (ch < c4) Y4[(size_t)row * ldy4 + ch] = act >= 0 ? act_fwd4(acc[q], act) : acc[q];
       }
     }
+    row = row_n;
+    s = s_n;
+    len = len_n;
   }
 }
 
@@ -109,8 +143,9 @@ __device__ __forceinline__ void tile_gemm(const float* __restrict__ Ys, int ys_l
   }
 }
 
-// Stage T rows of the tile into Ys (row stride ys_ld): aggregated (AGG) or
-// loaded directly from X.
+// Stage T rows of the tile into Ys (row stride ys_ld): aggregated (AGG; a
+// group of LPR lanes per row, next-row extent prefetched) or loaded directly
+// from X.
 template <int LPR, int VPL, bool AGG>
 __device__ __forceinline__ void stage_tile(const int* __restrict__ rp, const int* __restrict__ col,
                                            const float* __restrict__ val, const int* __restrict__ rows,
@@ -121,15 +156,22 @@ __device__ __forceinline__ void stage_tile(const int* __restrict__ rp, const int
     const int lane = threadIdx.x & 31;
     const int gl = lane & (LPR - 1);
     const int grp = threadIdx.x / LPR;
+    auto row_of = [&](int r) {
+      const int i = t0 + r;
+      return (r < T && i < n_rows) ? (rows ? __ldg(rows + i) : i) : -1;
+    };
+    int s, len;
+    row_extent(rp, row_of(grp), s, len);
     for (int r0 = 0; r0 < T; r0 += NG) {
       const int r = r0 + grp;
-      const int i = t0 + r;
-      int row = -1;
-      if (r < T && i < n_rows) row = rows ? __ldg(rows + i) : i;
+      int s_n, len_n;
+      row_extent(rp, row_of(r + NG), s_n, len_n);
       float4 acc[VPL];
 #pragma unroll
       for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      aggregate_row<LPR, VPL>(rp, col, val, row, X4, ldx4, c4, gl, acc);
+      aggregate_span<LPR, VPL>(col, val, s, len, X4, ldx4, c4, gl, acc);
+      s = s_n;
+      len = len_n;
       if (r < T) {
         float4* dst = reinterpret_cast<float4*>(Ys + r * ys_ld);
 #pragma unroll
@@ -154,7 +196,8 @@ __device__ __forceinline__ void stage_tile(const int* __restrict__ rp, const int
 }
 
 // Forward layer with the dense transform fused: H[r] = act((A[r,:]·X)·W)
-// (AGG) or H[r] = act(X[r]·W) (!AGG, the hoisted dense transform).
+// (AGG) or H[r] = act(X[r]·W) (!AGG, the hoisted dense transform); with
+// W == nullptr (AGG only) H[r] = act(A[r,:]·X).
 template <int LPR, int VPL, bool AGG, int RPT>
 __global__ void __launch_bounds__(NT) k_fwd_gemm(const int* __restrict__ rp, const int* __restrict__ col,
                                                  const float* __restrict__ val, const int* __restrict__ rows,
@@ -165,9 +208,10 @@ __global__ void __launch_bounds__(NT) k_fwd_gemm(const int* __restrict__ rp, con
   const int ld_in = (d_in + 3) & ~3;
   const int ld_out = (d_out + 3) & ~3;
   const int ys_ld = ld_in + 4;
+  const int w_floats = W ? d_in * ld_out : 0;
   float* Ws = smem;                     // d_in × ld_out
-  float* Ys = smem + d_in * ld_out;     // T × ys_ld
-  {
+  float* Ys = smem + w_floats;          // T × ys_ld
+  if (W) {
     const float4* W4 = reinterpret_cast<const float4*>(W);
     float4* Ws4 = reinterpret_cast<float4*>(Ws);
     for (int idx = threadIdx.x; idx < d_in * ld_out / 4; idx += NT) Ws4[idx] = __ldg(W4 + idx);
@@ -184,7 +228,17 @@ __global__ void __launch_bounds__(NT) k_fwd_gemm(const int* __restrict__ rp, con
     stage_tile<LPR, VPL, AGG>(rp, col, val, rows, n_rows, t0, T, reinterpret_cast<const float4*>(X), ldx / 4,
                               c4i, Ys, ys_ld);
     __syncthreads();
-    if (rpt > 0) {
+    if (!W) {
+      for (int idx = threadIdx.x; idx < T * c4i; idx += NT) {
+        const int r = idx / c4i, ch = idx - r * c4i;
+        const int i = t0 + r;
+        if (i < n_rows) {
+          const int row = rows ? __ldg(rows + i) : i;
+          reinterpret_cast<float4*>(H + (size_t)row * ldh)[ch] =
+              act_fwd4(reinterpret_cast<const float4*>(Ys + r * ys_ld)[ch], act);
+        }
+      }
+    } else if (rpt > 0) {
       float4 acc[RPT];
       tile_gemm<RPT>(Ys, ys_ld, Ws, ld_out, d_in, trg, RG, tc, rpt, acc);
 #pragma unroll
@@ -315,25 +369,59 @@ __global__ void __launch_bounds__(NT) k_bwd(const int* __restrict__ rp, const in
 // accumulators each and are combined in a fixed order.  With w != null the
 // SGD update w -= lr·out is fused (runtime.py:359-360).
 constexpr int RED_T = 1024;
-__global__ void __launch_bounds__(RED_T) k_reduce4(const float4* __restrict__ partials, int n_slots,
+constexpr int RED_SPB = 64;  // slots folded per level-1 block
+
+// Level 1 (many SMs): block (bx, by) folds slots [by*SPB, by*SPB+SPB) of its 64
+// chunks and writes the fixed-order sum back IN PLACE into slot by*SPB.
+__global__ void __launch_bounds__(RED_T) k_reduce_l1(float4* __restrict__ partials, int n_slots, long long size4) {
+  __shared__ float4 red[16][64];
+  const int lane = threadIdx.x & 63, grp = threadIdx.x >> 6;
+  const long long chunk = blockIdx.x * 64LL + lane;
+  const int s0 = blockIdx.y * RED_SPB;
+  const int s1 = min(n_slots, s0 + RED_SPB);
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, c = a, d = a;
+  if (chunk < size4) {
+    // 4 slots per group: s0 + grp + 16*j, j < 4 (independent loads)
+    const int b0 = s0 + grp;
+    if (b0 < s1) a = partials[(size_t)b0 * size4 + chunk];
+    if (b0 + 16 < s1) b = partials[(size_t)(b0 + 16) * size4 + chunk];
+    if (b0 + 32 < s1) c = partials[(size_t)(b0 + 32) * size4 + chunk];
+    if (b0 + 48 < s1) d = partials[(size_t)(b0 + 48) * size4 + chunk];
+  }
+  red[grp][lane] = make_float4(a.x + b.x + c.x + d.x, a.y + b.y + c.y + d.y, a.z + b.z + c.z + d.z,
+                               a.w + b.w + c.w + d.w);
+  __syncthreads();  // every read of this block's slot range is done before the in-place write
+  if (grp == 0 && chunk < size4) {
+    float4 t = red[0][lane];
+#pragma unroll
+    for (int g = 1; g < 16; ++g) {
+      t.x += red[g][lane].x; t.y += red[g][lane].y; t.z += red[g][lane].z; t.w += red[g][lane].w;
+    }
+    partials[(size_t)s0 * size4 + chunk] = t;
+  }
+}
+
+// Level 2 (or the only level): fold slots 0, stride, 2*stride, ... (< n_slots).
+__global__ void __launch_bounds__(RED_T) k_reduce4(const float4* __restrict__ partials, int n_slots, int stride,
                                                   long long size4, float4* __restrict__ out, int accumulate,
                                                   float4* __restrict__ w, float lr) {
   __shared__ float4 red[16][64];
   const int lane = threadIdx.x & 63, grp = threadIdx.x >> 6;
   const long long chunk = blockIdx.x * 64LL + lane;
-  // 8 independent accumulation chains per thread (slots grp + 16*(8*j + c)),
+  const int n_fold = (n_slots + stride - 1) / stride;  // slots 0, stride, 2*stride, ...
+  // 8 independent accumulation chains per thread (folded slots grp + 16*(8*j + c)),
   // combined in a fixed order: few dependent L2 round trips, deterministic.
   constexpr int CH = 8;
   float4 s[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) s[c] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (chunk < size4) {
-    for (int b0 = grp; b0 < n_slots; b0 += 16 * CH) {
+    for (int b0 = grp; b0 < n_fold; b0 += 16 * CH) {
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const int b = b0 + 16 * c;
-        if (b < n_slots) {
-          const float4 u = __ldg(partials + (size_t)b * size4 + chunk);
+        if (b < n_fold) {
+          const float4 u = __ldg(partials + (size_t)b * stride * size4 + chunk);
           s[c].x += u.x; s[c].y += u.y; s[c].z += u.z; s[c].w += u.w;
         }
       }
@@ -488,7 +576,7 @@ int launch_fwd_gemm(bool agg, const int32_t* row_ptr, const int32_t* col, const 
   const int T = tile_rows(d_out, s.lpr, &rpt);
   FwdFn fn = agg ? pick_fwd<true>(s, rpt) : pick_fwd<false>(s, rpt);
   GCNB_REQUIRE(fn != nullptr, "%s: unsupported width %d", what, d_in);
-  const size_t smem = sizeof(float) * ((size_t)d_in * round4(d_out) + (size_t)T * (round4(d_in) + 4));
+  const size_t smem = sizeof(float) * ((w ? (size_t)d_in * round4(d_out) : 0) + (size_t)T * (round4(d_in) + 4));
   GCNB_REQUIRE(smem <= 227 * 1024, "%s: tile does not fit shared memory", what);
   const int grid = occupancy_grid(reinterpret_cast<const void*>(fn), smem, (n_rows + T - 1) / T);
   fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, x, ldx, d_in, w, d_out, h, ldh, act, T);
@@ -533,7 +621,7 @@ extern "C" int gcnb_fwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
   GCNB_REQUIRE(aligned16(x) && aligned16(h) && (!w || aligned16(w)), "fwd layer: operands must be 16-byte aligned");
   if (n_rows == 0) return GCNB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  if (!w) {
+  if (!w) {  // aggregate-only: register path, no tile (no barrier, full occupancy)
     const AggShape s = agg_shape(d_in);
     AggFn fn = pick_agg(s);
     const int rows_per_block = NT / s.lpr;
@@ -600,9 +688,19 @@ extern "C" int gcnb_reduce_sgd_f32(const float* partials, int32_t n_slots, int64
   if (size == 0) return GCNB_OK;
   const long long size4 = size / 4;
   const int grid = (int)((size4 + 63) / 64);
-  k_reduce4<<<grid, RED_T, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4*>(partials), n_slots, size4,
-                                                      reinterpret_cast<float4*>(out), accumulate,
-                                                      reinterpret_cast<float4*>(w), lr);
+  cudaStream_t st = (cudaStream_t)stream;
+  int stride = 1;
+  if (n_slots > RED_SPB) {
+    // spread the slot fold over many SMs first (one SM's L2 bandwidth would
+    // otherwise bound a ~1 MB partial read), folding in place
+    const dim3 g1(grid, (n_slots + RED_SPB - 1) / RED_SPB);
+    k_reduce_l1<<<g1, RED_T, 0, st>>>(const_cast<float4*>(reinterpret_cast<const float4*>(partials)), n_slots,
+                                       size4);
+    GCNB_AFTER_LAUNCH("reduce partials (level 1)");
+    stride = RED_SPB;
+  }
+  k_reduce4<<<grid, RED_T, 0, st>>>(reinterpret_cast<const float4*>(partials), n_slots, stride, size4,
+                                    reinterpret_cast<float4*>(out), accumulate, reinterpret_cast<float4*>(w), lr);
   GCNB_AFTER_LAUNCH(w ? "reduce partials + sgd" : "reduce partials");
   return GCNB_OK;
 }

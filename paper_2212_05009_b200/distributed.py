@@ -78,8 +78,10 @@ def arena_layout(n_own: int, r_fwd: int, r_bwd: int, dims, transform_first, p: i
     take("slots", 2 * p * slot * 4)
     take("flags_halo", 8 * p)
     take("flags_ar", 8 * p)
+    take("flags_bar", 8 * p)
     take("expected_halo", 8 * p)
     take("expected_ar", 8 * p)
+    take("expected_bar", 8 * p)
     take("counter", 16)
     take("err", 16)
     off["_total"] = cur
@@ -233,6 +235,8 @@ class DistributedTrainer:
         self.flags_ar = a.tensor("flags_ar", (p,), torch.int64)
         self.expected_halo = a.tensor("expected_halo", (p,), torch.int64)
         self.expected_ar = a.tensor("expected_ar", (p,), torch.int64)
+        self.flags_bar = a.tensor("flags_bar", (p,), torch.int64)
+        self.expected_bar = a.tensor("expected_bar", (p,), torch.int64)
         self.counter = a.tensor("counter", (4,), torch.int32)
         self.err = a.tensor("err", (4,), torch.int32)
         self.slot = self.off["_slot"]
@@ -262,6 +266,7 @@ class DistributedTrainer:
                         for r in range(p)] for q in (0, 1)]
         self.ar_flag = [self.peer_base[r] + infos[r]["off"]["flags_ar"] + 8 * me for r in range(p)]
         self.ar_srcs = [r for r in range(p) if r != me]
+        self.bar_flag = [self.peer_base[r] + infos[r]["off"]["flags_bar"] + 8 * me for r in range(p) if r != me]
         torch.cuda.synchronize(device)
         dist.barrier()
         self.graphs = {}
@@ -314,6 +319,13 @@ class DistributedTrainer:
             st.dw_total[k] = st.dw_sum[k]
         st._has_trace = st._has_grad = True
 
+    def device_barrier(self) -> None:
+        """All ranks' streams reach this point before any continues (doorbells, no host sync)."""
+        if self.p == 1:
+            return
+        _lib.call("gcnb_signal_peers", _lib.ptr_array(self.bar_flag), len(self.bar_flag), self.st.stream())
+        self._wait(self.flags_bar, self.expected_bar, self.ar_srcs)
+
     def capture(self, key, parity: int, comm: bool = True, timer=None) -> None:
         import torch
 
@@ -356,8 +368,12 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun --nproc-per-node {args.gpus}")
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
-    dist.init_process_group(backend="cpu:gloo,cuda:nccl", device_id=device)
-    wl = build_workload(args.workload, args.seed)
+    dist.init_process_group(backend="gloo")  # rendezvous + tiny host collectives only
+    if rank == 0:  # rank 0 generates (and caches) the graph; the others load it
+        wl = build_workload(args.workload, args.seed)
+    dist.barrier()
+    if rank != 0:
+        wl = build_workload(args.workload, args.seed)
     n = wl["n"]
     t0 = time.perf_counter()
     # rank 0 partitions (host preprocessing) and broadcasts the owner array
@@ -409,6 +425,7 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
         for i in range(args.steps):
             q = (start_parity + i) % 2
             flush.zero_()
+            tr.device_barrier()  # all ranks start the step together (not timed)
             evs[i][0].record()
             tr.graphs[q].replay()
             evs[i][1].record()
@@ -422,6 +439,7 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
     cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for i in range(args.steps):
         flush.zero_()
+        tr.device_barrier()
         cev[i][0].record()
         tr.graphs["compute"].replay()
         cev[i][1].record()
@@ -443,10 +461,10 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
         par ^= 1
     tr.check()
     e2e_ms = 1e3 * float(np.mean(e2e)) if e2e else float("nan")
-    vals = torch.tensor([ms_rank, ms_compute, e2e_ms], dtype=torch.float64, device=device)
+    vals = torch.tensor([ms_rank, ms_compute, e2e_ms], dtype=torch.float64)
     dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     halo = torch.tensor([halo_bytes_per_epoch(tr.layout, st.dims, st.transform_first),
-                         reference_words_per_epoch(tr.layout, st.dims)], dtype=torch.float64, device=device)
+                         reference_words_per_epoch(tr.layout, st.dims)], dtype=torch.float64)
     dist.all_reduce(halo, op=dist.ReduceOp.SUM)
     peak, peak_kind = measured_peaks()
     compute_rows = [r for r in rows if not r[0].startswith(("pack", "allreduce"))]
@@ -480,8 +498,7 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
         "cpu_baseline": None,
         "clocks": clk,
     }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     dist.barrier()
     tr.close()
     dist.destroy_process_group()
+    return line if rank == 0 else None

@@ -30,15 +30,29 @@ from .sparse import CsrMatrix
 
 
 def _csr_from_pairs(n: int, rows: np.ndarray, cols: np.ndarray) -> CsrMatrix:
-    order = np.lexsort((cols, rows))
-    rows, cols = rows[order], cols[order]
+    """Distinct (row, col) pairs → unit-valued CSR (one int64 key sort)."""
+    keys = np.asarray(rows, dtype=np.int64) * n + np.asarray(cols, dtype=np.int64)
+    keys.sort()
+    rows = keys // n
     rp = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
-    return CsrMatrix(n, n, rp, cols, np.ones(len(cols)))
+    return CsrMatrix(n, n, rp, keys - rows * n, np.ones(len(keys)))
+
+
+def _uniq(x: np.ndarray) -> np.ndarray:
+    """Sorted distinct values (sort + adjacent compare; numpy 2's hash-based
+    np.unique is ~5x slower on 10^7-10^8 int64 keys)."""
+    x = np.sort(x)
+    if len(x) == 0:
+        return x
+    keep = np.empty(len(x), dtype=bool)
+    keep[0] = True
+    np.not_equal(x[1:], x[:-1], out=keep[1:])
+    return x[keep]
 
 
 def _exact_count(keys: np.ndarray, m: int, rng) -> np.ndarray:
-    keys = np.unique(keys)
+    keys = _uniq(keys)
     if len(keys) < m:
         raise RuntimeError(f"generator produced {len(keys)} distinct entries, need {m}")
     return np.sort(keys[rng.choice(len(keys), size=m, replace=False)])
@@ -94,20 +108,33 @@ def products(seed: int = 0, n: int = 2_449_029, pairs: int = 61_859_140, blocks:
     bounds = np.searchsorted(block, np.arange(blocks + 1))
     prop = rng.lognormal(0.0, sigma, n)
     cum = np.cumsum(prop)
-    k = int(pairs * 1.04)
-    u = np.minimum(np.searchsorted(cum, rng.random(k) * cum[-1]), n - 1)
-    same = rng.random(k) < intra
-    # intra-block partner: inverse-CDF draw restricted to u's block
-    lo = bounds[block[u]]
-    hi = bounds[block[u] + 1]
-    c_lo = np.where(lo > 0, cum[lo - 1], 0.0)
-    c_hi = cum[hi - 1]
-    w_in = np.minimum(np.searchsorted(cum, c_lo + rng.random(k) * (c_hi - c_lo)), n - 1)
-    w_any = np.minimum(np.searchsorted(cum, rng.random(k) * cum[-1]), n - 1)
-    w = np.where(same, w_in, w_any)
-    keep = u != w
-    a, b = np.minimum(u[keep], w[keep]), np.maximum(u[keep], w[keep])
-    keys = _exact_count(a * n + b, pairs, rng)
+
+    def inv_cdf(x):
+        # sorted queries make the binary searches cache-friendly; the draws stay i.i.d.
+        order = np.argsort(x)
+        out = np.empty(len(x), dtype=np.int64)
+        out[order] = np.minimum(np.searchsorted(cum, x[order]), n - 1)
+        return out
+
+    def draw(k):
+        u = inv_cdf(rng.random(k) * cum[-1])
+        same = rng.random(k) < intra
+        # intra-block partner: inverse-CDF draw restricted to u's block
+        lo = bounds[block[u]]
+        hi = bounds[block[u] + 1]
+        c_lo = np.where(lo > 0, cum[np.maximum(lo - 1, 0)], 0.0)
+        c_hi = cum[hi - 1]
+        w_in = inv_cdf(c_lo + rng.random(k) * (c_hi - c_lo))
+        w_any = inv_cdf(rng.random(k) * cum[-1])
+        w = np.where(same, w_in, w_any)
+        keep = u != w
+        a, b = np.minimum(u[keep], w[keep]), np.maximum(u[keep], w[keep])
+        return _uniq(a * n + b)
+
+    keys = draw(int(pairs * 1.08))
+    while len(keys) < pairs:  # heavy vertices repeat pairs: top up until enough distinct pairs
+        keys = _uniq(np.concatenate([keys, draw(int((pairs - len(keys)) * 1.5) + 1024)]))
+    keys = _exact_count(keys, pairs, rng)
     perm = rng.permutation(n)
     x, y = perm[keys // n], perm[keys % n]
     return _csr_from_pairs(n, np.concatenate([x, y]), np.concatenate([y, x]))

@@ -32,7 +32,7 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank)))
     torch.cuda.set_device(dev)
-    dist.init_process_group(backend="cpu:gloo,cuda:nccl", device_id=dev)
+    dist.init_process_group(backend="gloo")
     n, dims = args.n, (12, 16, 6)
     raw = o.random_directed(n, 0.002, 5) if args.directed else o.random_undirected(n, 0.002, 5)
     a_hat = gb.normalize_adjacency(gb.CsrMatrix(n, n, raw.row_offsets, raw.col_indices, raw.values))

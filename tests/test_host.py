@@ -223,3 +223,22 @@ class TestHostTypes:
         assert np.array_equal(sub.to_dense(), want.astype(float))
         sub = gb.induced_pattern(a, batch, add_diagonal=False)
         assert np.array_equal(sub.to_dense(), (raw.to_dense()[np.ix_(batch, batch)] != 0).astype(float))
+
+
+class TestNormalizeFastPath:
+    @pytest.mark.parametrize("seed", range(4))
+    def test_existing_diagonal_and_weights_bit_identical(self, seed):
+        rng = np.random.default_rng(seed)
+        d = (rng.random((30, 30)) < 0.2) * rng.uniform(0.5, 2.0, (30, 30))
+        d[np.arange(0, 30, 3), np.arange(0, 30, 3)] = 0.75  # some rows already hold a self loop
+        a = gb.CsrMatrix.from_dense(d)
+        mine = gb.normalize_adjacency(a)
+        want = o.normalize_adjacency(o.Csr(30, 30, a.row_offsets, a.col_indices, a.values))
+        assert np.array_equal(mine.row_offsets, want.row_offsets)
+        assert np.array_equal(mine.col_indices, want.col_indices)
+        assert np.array_equal(mine.values, want.values)
+
+    def test_empty_rows_get_self_loops(self):
+        a = gb.CsrMatrix(4, 4, [0, 0, 1, 1, 1], [3], [2.0])
+        t = gb.normalize_adjacency(a)
+        assert t.has_full_diagonal() and t.nnz == 5
