@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--locality", default="on", choices=("on", "off"),
+                    help="lay own rows out by label-propagation community (layout only; results unchanged)")
     ap.add_argument("--kernels-only", action="store_true",
                     help="skip the e2e and CPU-baseline legs (for ncu launch lists)")
     return ap.parse_args()
@@ -264,7 +266,10 @@ def run_single(args):
     wl = build_workload(args.workload, args.seed)
     n = wl["n"]
     owner = np.zeros(n, dtype=np.int64)
-    states = gb.scatter(wl["a_hat"], wl["h0"], owner, wl["model"], directed=wl["directed"], p=1, device=dev)
+    t_loc = time.perf_counter()
+    states = gb.scatter(wl["a_hat"], wl["h0"], owner, wl["model"], directed=wl["directed"], p=1, device=dev,
+                        locality=args.locality == "on")
+    t_loc = time.perf_counter() - t_loc
     runner = EpochRunner(states, wl["labels"])
 
     c0 = _lib.launch_count()
@@ -342,7 +347,8 @@ def run_single(args):
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": wl["name"], "n": n, "nnz_ahat": wl["nnz"], "dims": list(wl["dims"]),
-                   "directed": wl["directed"], "partition": "p=1", "l2": "flushed (512 MiB write) before every step",
+                   "directed": wl["directed"], "partition": "p=1", "locality": args.locality,
+                   "scatter_s": round(t_loc, 2), "l2": "flushed (512 MiB write) before every step",
                    "graph": not args.no_graph, "seed": args.seed},
         "e2e": {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "loss_last": m[0].loss if m[0] is not None else None},

@@ -141,7 +141,13 @@ int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* 
                        const float* g, int32_t ldg, int32_t d_k,
                        const float* h_prev, int32_t ldhp, int32_t d_prev,
                        const float* w, float* g_prev, int32_t ldgp, int32_t act,
-                       float* dw_partials, void* stream);
+                       float* dw_partials, float* workspace, void* stream);
+/* Row stride (floats) of the optional `workspace` of gcnb_bwd_layer_f32 for
+ * these widths, or 0 when the fused single-kernel form is always used.  With a
+ * workspace of (own rows) × ld floats, large-ΔW layers run as an aggregation
+ * kernel (agg → workspace, full occupancy) plus a dense epilogue kernel;
+ * results are identical (same accumulation orders). */
+int gcnb_bwd_workspace_ld(int32_t d_prev, int32_t d_k, int32_t* ld_out);
 
 /* out[j] = (accumulate ? out[j] : 0) + Σ_{s < n_slots} partials[s*size + j],
  * summed in a fixed (deterministic) order, j < size, size % 4 == 0.  The

@@ -52,7 +52,8 @@ _SIGNATURES = {
     "gcnb_bwd_layer_f32": (
         _c_int,
         [_vp, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp,
-         _vp]),
+         _vp, _vp]),
+    "gcnb_bwd_workspace_ld": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_int)]),
     "gcnb_reduce_partials_f32": (_c_int, [_vp, _c_int, _c_i64, _vp, _c_int, _vp]),
     "gcnb_reduce_sgd_f32": (_c_int, [_vp, _c_int, _c_i64, _vp, _c_int, _vp, _f32, _vp]),
     "gcnb_loss_scratch_doubles": (_c_int, []),
@@ -137,6 +138,12 @@ def launch_count() -> int:
 def bwd_grid(n_rows: int, d_prev: int, d_k: int, with_gprev: bool) -> int:
     out = ctypes.c_int32(0)
     call("gcnb_bwd_grid", n_rows, d_prev, d_k, int(with_gprev), ctypes.byref(out))
+    return int(out.value)
+
+
+def bwd_workspace_ld(d_prev: int, d_k: int) -> int:
+    out = ctypes.c_int32(0)
+    call("gcnb_bwd_workspace_ld", d_prev, d_k, ctypes.byref(out))
     return int(out.value)
 
 

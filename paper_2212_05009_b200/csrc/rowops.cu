@@ -22,6 +22,21 @@
 
 namespace gcnb {
 
+// 16-byte read-only gather as a volatile asm: volatile loads keep their program
+// order, so a batch of them is issued back to back (all in flight) before the
+// dependent FMAs — the compiler otherwise interleaves load→fma pairs to save
+// registers and keeps one gather in flight per lane.
+__device__ __forceinline__ float4 ldg_batch(const float4* p, bool pred) {
+  float4 v;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\tmov.b32 %2, 0;\n\tmov.b32 %3, 0;\n\t"
+      "@q ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p), "r"((int)pred));
+  return v;
+}
+
 // Row extent [s, s+len) of CSR row `row` (row < 0: empty).
 __device__ __forceinline__ void row_extent(const int* __restrict__ rp, int row, int& s, int& len) {
   s = 0;
@@ -57,17 +72,90 @@ __device__ __forceinline__ void aggregate_span(const int* __restrict__ col, cons
       vn = __ldg(val + s + base + LPR + gl);
     }
     const int cnt = min(LPR, maxlen - base);
-#pragma unroll 8
-    for (int t = 0; t < cnt; ++t) {
-      const int c = __shfl_sync(0xffffffffu, cj, t, LPR);
-      const float v = __shfl_sync(0xffffffffu, vj, t, LPR);
-      if (base + t < len) {
+    // Issue U independent row gathers into distinct registers before any is
+    // consumed: a load→fma→load chain would keep only one gather in flight
+    // per lane (the compiler reuses the destination registers otherwise).
+    constexpr int U = LPR < 8 ? LPR : 8;
+    for (int t0 = 0; t0 < cnt; t0 += U) {
+      float4 xv[U][VPL];
+      float vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u;
+        const int c = __shfl_sync(0xffffffffu, cj, t & (LPR - 1), LPR);
+        const float v = __shfl_sync(0xffffffffu, vj, t & (LPR - 1), LPR);
+        const bool ok = t < cnt && base + t < len;
+        vv[u] = ok ? v : 0.0f;
         const float4* xr = X4 + (size_t)c * ldx4;
 #pragma unroll
         for (int q = 0; q < VPL; ++q) {
           const int ch = gl + q * LPR;
-          if (ch < c4) acc[q] = fma4(v, __ldg(xr + ch), acc[q]);
+          xv[u][q] = ldg_batch(xr + ch, ok && ch < c4);
         }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) acc[q] = fma4(vv[u], xv[u][q], acc[q]);
+      }
+    }
+    cj = cn;
+    vj = vn;
+  }
+}
+
+// The same aggregation with the U gathers of a batch issued as cp.async into a
+// per-warp shared-memory staging slot (stage: [U][VPL][32 lanes] float4): the
+// copies are memory operations the scheduler cannot sink next to their uses,
+// so U gathers per lane are genuinely in flight, at no register cost.  Each
+// lane reads back only the slot it filled itself (no warp barrier needed).
+__device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  const int sz = pred ? 16 : 0;  // src-size 0: zero-fill, no global access
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem_src), "r"(sz) : "memory");
+}
+
+template <int LPR, int VPL, int U>
+__device__ __forceinline__ void aggregate_span_cp(const int* __restrict__ col, const float* __restrict__ val, int s,
+                                                  int len, const float4* __restrict__ X4, int ldx4, int c4, int gl,
+                                                  float4 (&acc)[VPL], float4* __restrict__ stage) {
+  const int lane = threadIdx.x & 31;
+  const int maxlen = __reduce_max_sync(0xffffffffu, len);
+  int cj = 0;
+  float vj = 0.0f;
+  if (gl < len) {
+    cj = __ldg(col + s + gl);
+    vj = __ldg(val + s + gl);
+  }
+  for (int base = 0; base < maxlen; base += LPR) {
+    int cn = 0;
+    float vn = 0.0f;
+    if (base + LPR + gl < len) {
+      cn = __ldg(col + s + base + LPR + gl);
+      vn = __ldg(val + s + base + LPR + gl);
+    }
+    const int cnt = min(LPR, maxlen - base);
+    for (int t0 = 0; t0 < cnt; t0 += U) {
+      float vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u;
+        const int c = __shfl_sync(0xffffffffu, cj, t & (LPR - 1), LPR);
+        const float v = __shfl_sync(0xffffffffu, vj, t & (LPR - 1), LPR);
+        const bool ok = t < cnt && base + t < len;
+        vv[u] = ok ? v : 0.0f;
+        const float4* xr = X4 + (size_t)(ok ? c : 0) * ldx4;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const int ch = gl + q * LPR;
+          cp_async_16(stage + (u * VPL + q) * 32 + lane, xr + ch, ok && ch < c4);
+        }
+      }
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) acc[q] = fma4(vv[u], stage[(u * VPL + q) * 32 + lane], acc[q]);
       }
     }
     cj = cn;
@@ -99,6 +187,9 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
   const int warp_global = (blockIdx.x * NT + threadIdx.x) >> 5;
   const int n_warps = gridDim.x * WARPS;
   const int stride = n_warps * GPW;
+  constexpr int U = LPR < 8 ? LPR : 8;
+  extern __shared__ __align__(16) float4 stage_all[];
+  float4* stage = stage_all + (threadIdx.x >> 5) * (U * VPL * 32);
   auto row_of = [&](int i) { return i < n_rows ? (rows ? __ldg(rows + i) : i) : -1; };
   int row = row_of(warp_global * GPW + gw);
   int s, len;
@@ -111,7 +202,7 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
     float4 acc[VPL];
 #pragma unroll
     for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    aggregate_span<LPR, VPL>(col, val, s, len, X4, ldx4, c4, gl, acc);
+    aggregate_span_cp<LPR, VPL, U>(col, val, s, len, X4, ldx4, c4, gl, acc, stage);
     if (row >= 0) {
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
@@ -307,8 +398,12 @@ __global__ void __launch_bounds__(NT) k_bwd(const int* __restrict__ rp, const in
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int t0 = tile * T;
     const int tv = min(T, n_rows - t0);
-    stage_tile<LPR, VPL, true>(rp, col, val, rows, n_rows, t0, T, reinterpret_cast<const float4*>(G), ldg / 4,
-                               c4k, As, as_ld);
+    if (rp)
+      stage_tile<LPR, VPL, true>(rp, col, val, rows, n_rows, t0, T, reinterpret_cast<const float4*>(G), ldg / 4,
+                                 c4k, As, as_ld);
+    else  // split mode: G already holds agg = A_back·G (own-row positions)
+      stage_tile<LPR, VPL, false>(nullptr, nullptr, nullptr, rows, n_rows, t0, T,
+                                  reinterpret_cast<const float4*>(G), ldg / 4, c4k, As, as_ld);
     stage_tile<LPR, VPL, false>(nullptr, nullptr, nullptr, rows, n_rows, t0, T,
                                 reinterpret_cast<const float4*>(Hp), ldhp / 4, c4p, Hs, hs_ld);
     __syncthreads();
@@ -530,6 +625,10 @@ BwdFn pick_bwd_ipt(AggShape s, bool gp, int rpt) {
   return pick_bwd_t<IPT, false, 4>(s);  // no S-GEMM without G_prev: RPT is unused
 }
 
+// Large ΔW tiles make the fused backward kernel register-bound (2 blocks/SM):
+// then the aggregation and the dense epilogue run as two kernels.
+bool bwd_split(int d_prev, int d_k) { return (long)d_prev * round4(d_k) > 2048; }
+
 struct BwdPlan {
   BwdFn fn;
   int T;
@@ -548,6 +647,7 @@ int bwd_plan(int n_rows, int d_prev, int d_k, bool with_gp, BwdPlan* out) {
   BwdFn fn = nullptr;
   if (ipt <= 1) fn = pick_bwd_ipt<1>(s, with_gp, rpt);
   else if (ipt <= 4) fn = pick_bwd_ipt<4>(s, with_gp, rpt);
+  else if (ipt <= 8) fn = pick_bwd_ipt<8>(s, with_gp, rpt);
   else if (ipt <= 16) fn = pick_bwd_ipt<16>(s, with_gp, rpt);
   else if (ipt <= 32) fn = pick_bwd_ipt<32>(s, with_gp, rpt);
   GCNB_REQUIRE(fn != nullptr, "bwd layer: unsupported widths d_prev=%d d_k=%d", d_prev, d_k);
@@ -565,6 +665,28 @@ int bwd_plan(int n_rows, int d_prev, int d_k, bool with_gp, BwdPlan* out) {
 int check_csr_args(const int32_t* row_ptr, const int32_t* col, const float* val, int32_t n_rows) {
   GCNB_REQUIRE(n_rows >= 0, "n_rows must be >= 0");
   GCNB_REQUIRE(n_rows == 0 || (row_ptr && col && val), "CSR arrays must be non-null");
+  return GCNB_OK;
+}
+
+int launch_agg(const int32_t* row_ptr, const int32_t* col, const float* val, const int32_t* rows, int32_t n_rows,
+               const float* x, int32_t ldx, int32_t d, float* y, int32_t ldy, int32_t act, cudaStream_t st,
+               const char* what) {
+  const AggShape s = agg_shape(d);
+  AggFn fn = pick_agg(s);
+  const size_t smem = (size_t)WARPS * std::min(s.lpr, 8) * s.vpl * 32 * sizeof(float4);
+  const int rows_per_block = NT / s.lpr;
+  int per_sm = 0;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn), NT, smem) !=
+          cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  const int grid = std::max(1, std::min((n_rows + rows_per_block - 1) / rows_per_block, num_sms() * per_sm));
+  fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, reinterpret_cast<const float4*>(x), ldx / 4,
+                             round4(d) / 4, reinterpret_cast<float4*>(y), ldy / 4, act);
+  GCNB_AFTER_LAUNCH(what);
   return GCNB_OK;
 }
 
@@ -598,14 +720,7 @@ extern "C" int gcnb_spmm_f32(const int32_t* row_ptr, const int32_t* col, const f
                "spmm: row strides must be multiples of 4 and >= round4(d)");
   GCNB_REQUIRE(aligned16(x) && aligned16(y), "spmm: X and Y must be 16-byte aligned");
   if (n_rows == 0) return GCNB_OK;
-  const AggShape s = agg_shape(d);
-  AggFn fn = pick_agg(s);
-  const int rows_per_block = NT / s.lpr;
-  const int grid = std::max(1, std::min((n_rows + rows_per_block - 1) / rows_per_block, num_sms() * 8));
-  fn<<<grid, NT, 0, (cudaStream_t)stream>>>(row_ptr, col, val, rows, n_rows, reinterpret_cast<const float4*>(x),
-                                            ldx / 4, round4(d) / 4, reinterpret_cast<float4*>(y), ldy / 4, -1);
-  GCNB_AFTER_LAUNCH("spmm");
-  return GCNB_OK;
+  return launch_agg(row_ptr, col, val, rows, n_rows, x, ldx, d, y, ldy, -1, (cudaStream_t)stream, "spmm");
 }
 
 extern "C" int gcnb_fwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* val,
@@ -621,16 +736,8 @@ extern "C" int gcnb_fwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
   GCNB_REQUIRE(aligned16(x) && aligned16(h) && (!w || aligned16(w)), "fwd layer: operands must be 16-byte aligned");
   if (n_rows == 0) return GCNB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  if (!w) {  // aggregate-only: register path, no tile (no barrier, full occupancy)
-    const AggShape s = agg_shape(d_in);
-    AggFn fn = pick_agg(s);
-    const int rows_per_block = NT / s.lpr;
-    const int grid = std::max(1, std::min((n_rows + rows_per_block - 1) / rows_per_block, num_sms() * 8));
-    fn<<<grid, NT, 0, st>>>(row_ptr, col, val, rows, n_rows, reinterpret_cast<const float4*>(x), ldx / 4,
-                            round4(d_in) / 4, reinterpret_cast<float4*>(h), ldh / 4, act);
-    GCNB_AFTER_LAUNCH("fwd layer (aggregate)");
-    return GCNB_OK;
-  }
+  if (!w)  // aggregate-only: no tile (no barrier, full occupancy)
+    return launch_agg(row_ptr, col, val, rows, n_rows, x, ldx, d_in, h, ldh, act, st, "fwd layer (aggregate)");
   return launch_fwd_gemm(true, row_ptr, col, val, rows, n_rows, x, ldx, d_in, w, d_out, h, ldh, act, st,
                          "fwd layer (aggregate+transform)");
 }
@@ -659,7 +766,8 @@ extern "C" int gcnb_bwd_grid(int32_t n_rows, int32_t d_prev, int32_t d_k, int32_
 extern "C" int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* val,
                                   const int32_t* rows, int32_t n_rows, const float* g, int32_t ldg, int32_t d_k,
                                   const float* h_prev, int32_t ldhp, int32_t d_prev, const float* w,
-                                  float* g_prev, int32_t ldgp, int32_t act, float* dw_partials, void* stream) {
+                                  float* g_prev, int32_t ldgp, int32_t act, float* dw_partials, float* workspace,
+                                  void* stream) {
   if (int rc = check_csr_args(row_ptr, col, val, n_rows)) return rc;
   GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "bwd layer: unknown activation %d", act);
   GCNB_REQUIRE(d_prev >= 1 && d_prev <= 256 && d_k >= 1 && d_k <= 256, "bwd layer: widths out of range");
@@ -669,12 +777,31 @@ extern "C" int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
                "bwd layer: G_prev needs W and an aligned stride >= round4(d_prev)");
   GCNB_REQUIRE(g && h_prev && dw_partials && aligned16(g) && aligned16(h_prev) && aligned16(dw_partials),
                "bwd layer: operands must be non-null and 16-byte aligned");
+  GCNB_REQUIRE(!workspace || aligned16(workspace), "bwd layer: workspace must be 16-byte aligned");
   BwdPlan plan;
   if (int rc = bwd_plan(n_rows, d_prev, d_k, g_prev != nullptr, &plan)) return rc;
-  plan.fn<<<plan.grid, NT, plan.smem, (cudaStream_t)stream>>>(row_ptr, col, val, rows, n_rows, g, ldg, d_k, h_prev,
-                                                              ldhp, d_prev, w, g_prev, ldgp, act, dw_partials,
-                                                              plan.T);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (workspace && bwd_split(d_prev, d_k) && n_rows > 0) {
+    // split mode: the gather-bound aggregation runs at full occupancy (k_agg,
+    // cp.async staging), the register-heavy dense epilogue streams agg back
+    if (int rc = launch_agg(row_ptr, col, val, rows, n_rows, g, ldg, d_k, workspace, round4(d_k), -1, st,
+                            "bwd layer (aggregate)"))
+      return rc;
+    plan.fn<<<plan.grid, NT, plan.smem, st>>>(nullptr, nullptr, nullptr, rows, n_rows, workspace, round4(d_k), d_k,
+                                              h_prev, ldhp, d_prev, w, g_prev, ldgp, act, dw_partials, plan.T);
+    GCNB_AFTER_LAUNCH("bwd layer (dense epilogue)");
+    return GCNB_OK;
+  }
+  plan.fn<<<plan.grid, NT, plan.smem, st>>>(row_ptr, col, val, rows, n_rows, g, ldg, d_k, h_prev, ldhp, d_prev, w,
+                                            g_prev, ldgp, act, dw_partials, plan.T);
   GCNB_AFTER_LAUNCH("bwd layer");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_bwd_workspace_ld(int32_t d_prev, int32_t d_k, int32_t* ld_out) {
+  GCNB_REQUIRE(ld_out != nullptr, "bwd workspace: null output");
+  GCNB_REQUIRE(d_prev >= 1 && d_prev <= 256 && d_k >= 1 && d_k <= 256, "bwd workspace: widths out of range");
+  *ld_out = bwd_split(d_prev, d_k) ? round4(d_k) : 0;
   return GCNB_OK;
 }
 

@@ -123,7 +123,7 @@ class RankSchedule:
         return cnt
 
 
-def build_rank(a_hat, owner, p: int, rank: int, directed: bool):
+def build_rank(a_hat, owner, p: int, rank: int, directed: bool, row_labels=None):
     """Global plans + this rank's layout (every rank computes the same plans)."""
     plan_fwd = build_comm_plan(a_hat, owner, p)
     if directed:
@@ -131,7 +131,7 @@ def build_rank(a_hat, owner, p: int, rank: int, directed: bool):
         plan_bwd = build_comm_plan(a_bwd, owner, p)
     else:
         a_bwd, plan_bwd = a_hat, plan_fwd
-    layout = build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, rank)
+    layout = build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, rank, row_labels=row_labels)
     return plan_fwd, plan_bwd, layout
 
 
@@ -203,7 +203,10 @@ class Arena:
 class DistributedTrainer:
     """Full-batch training of this process's rank; collective over torch.distributed."""
 
-    def __init__(self, a_hat, h0, owner, p: int, model, labels, directed: bool, device, timeout_ms: int = 20000):
+    def __init__(self, a_hat, h0, owner, p: int, model, labels, directed: bool, device, timeout_ms: int = 20000,
+                 row_labels=None):
+        """row_labels: optional per-vertex community labels for the locality
+        layout of own rows (locality.py); None keeps ascending global ids."""
         import torch
         import torch.distributed as dist
 
@@ -213,7 +216,7 @@ class DistributedTrainer:
         self.p = p
         self.device = device
         self.timeout_ms = timeout_ms
-        plan_fwd, plan_bwd, layout = build_rank(a_hat, owner, p, self.rank, directed)
+        plan_fwd, plan_bwd, layout = build_rank(a_hat, owner, p, self.rank, directed, row_labels)
         self.layout = layout
         self.sched = RankSchedule(plan_fwd, plan_bwd, self.rank, len(model.dims) - 1)
         dims = tuple(int(d) for d in model.dims)
@@ -387,17 +390,18 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
             pi = partition_hypergraph(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1)
         else:
             pi = random_partition(wl["a_hat"].row_nnz(), PartitionConfig(p=world, seed=args.seed, epsilon=0.01))
-        box[0] = pi.assignment
+        labels = None
+        if args.locality == "on":
+            from .locality import community_labels
+
+            labels = community_labels(wl["a_hat"])
+        box[0] = (pi.assignment, labels)
     dist.broadcast_object_list(box, src=0)
-    owner = np.asarray(box[0], dtype=np.int64)
+    owner = np.asarray(box[0][0], dtype=np.int64)
+    row_labels = box[0][1]
     t_part = time.perf_counter() - t0
-
-    class _Pi:
-        assignment = owner
-
-    pi = _Pi()
-    tr = DistributedTrainer(wl["a_hat"], wl["h0"], pi.assignment, world, wl["model"], wl["labels"], wl["directed"],
-                            device)
+    tr = DistributedTrainer(wl["a_hat"], wl["h0"], owner, world, wl["model"], wl["labels"], wl["directed"],
+                            device, row_labels=row_labels)
     st = tr.st
     from . import _lib as L_
 
@@ -483,6 +487,7 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": wl["name"], "n": n, "nnz_ahat": wl["nnz"], "dims": list(wl["dims"]),
                    "directed": wl["directed"], "partition": args.partition, "partition_s": round(t_part, 2),
+                   "locality": args.locality,
                    "l2": "flushed (512 MiB write) before every step", "graph": True, "seed": args.seed,
                    "transport": "NVLink peer stores + doorbells (CUDA IPC), P2P allreduce"},
         "e2e": {"value": round(e2e_max, 4), "unit": UNIT,

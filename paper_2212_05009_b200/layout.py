@@ -143,8 +143,14 @@ def build_op_layout(a, plan: CommPlan, m: int, rows: np.ndarray, sort_rows: bool
                     send_dst, send_ptr, send_idx, dst_slot)
 
 
-def build_rank_layout(a_fwd, a_bwd, plan_fwd: CommPlan, plan_bwd: CommPlan, m: int) -> RankLayout:
+def build_rank_layout(a_fwd, a_bwd, plan_fwd: CommPlan, plan_bwd: CommPlan, m: int,
+                      row_labels: np.ndarray | None = None) -> RankLayout:
+    """Rank m's layout.  Own rows are in ascending global id (the reference's
+    order) unless `row_labels` (one community label per vertex) is given, in
+    which case they are laid out by (label, global id) for gather locality."""
     rows = plan_fwd.rows_of(m)
+    if row_labels is not None:
+        rows = rows[np.lexsort((rows, np.asarray(row_labels)[rows]))]
     fwd = build_op_layout(a_fwd, plan_fwd, m, rows)
     bwd = fwd if (a_bwd is a_fwd and plan_bwd is plan_fwd) else build_op_layout(a_bwd, plan_bwd, m, rows)
     return RankLayout(m, plan_fwd.p, rows, fwd, bwd)

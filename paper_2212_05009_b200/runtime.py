@@ -279,6 +279,12 @@ class ProcState:
                 slots = max(gi + gb, ga)
                 self.partials[k] = torch.zeros((slots, self.dims[k - 1] * devmem.ld_of(self.dims[k])),
                                                dtype=torch.float32, device=dev)
+            # split-mode workspace (agg rows) for large-ΔW layers (gcnb_bwd_workspace_ld)
+            self.bwd_ws = [None] * (L + 1)
+            for k in range(1, L + 1):
+                ld = _lib.bwd_workspace_ld(self.dims[k - 1], self.dims[k])
+                if ld:
+                    self.bwd_ws[k] = torch.zeros((max(n, 1), ld), dtype=torch.float32, device=dev)
             self.label = torch.full((max(n, 1),), -1, dtype=torch.int32, device=dev)
             self.loss_scratch = torch.zeros(_lib.loss_scratch_doubles(), dtype=torch.float64, device=dev)
             # the rank's NLL sum lives in the ΔW pack tail (it travels with the allreduce)
@@ -351,20 +357,28 @@ class ProcState:
         return torch.cuda.current_stream(self.device).cuda_stream
 
     def set_labels(self, labels) -> int:
-        """Upload this rank's label map; returns its labelled-row count."""
+        """Upload this rank's label map; returns its labelled-row count.  The
+        upload is skipped when the same (immutable) LabelSet is already resident."""
+        if getattr(self, "_labels_obj", None) is labels:
+            return self.n_labeled
         ids = np.asarray(labels.labeled_ids, dtype=np.int64)
         lab = np.asarray(labels.labels, dtype=np.int64)
         rows = self.global_rows
         lab_map = np.full(max(self.n_own, 1), -1, dtype=np.int32)
         if len(ids) and len(rows):
-            pos = np.searchsorted(rows, ids)
-            mine = (pos < len(rows)) & (rows[np.minimum(pos, len(rows) - 1)] == ids)
-            lab_map[pos[mine]] = lab[mine]
+            if not hasattr(self, "_row_order"):  # own rows may be in locality order
+                self._row_order = np.argsort(rows, kind="stable")
+                self._rows_sorted = rows[self._row_order]
+            srt = self._rows_sorted
+            pos = np.searchsorted(srt, ids)
+            mine = (pos < len(srt)) & (srt[np.minimum(pos, len(srt) - 1)] == ids)
+            lab_map[self._row_order[pos[mine]]] = lab[mine]
             count = int(mine.sum())
         else:
             count = 0
         self.label.copy_(torch.from_numpy(lab_map))
         self.n_labeled = count
+        self._labels_obj = labels
         return count
 
     def fwd_operand(self, k: int):
@@ -434,7 +448,8 @@ class ProcState:
             _lib.call("gcnb_bwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
                       op.csr.val.data_ptr(), sel, n_sel, g.data_ptr(), g.shape[1], dk, hp.data_ptr(), hp.shape[1],
                       dp, self.w[k].data_ptr(), 0 if gp is None else gp.data_ptr(),
-                      0 if gp is None else gp.shape[1], self.act, part.data_ptr(), self.stream())
+                      0 if gp is None else gp.shape[1], self.act, part.data_ptr(),
+                      0 if self.bwd_ws[k] is None else self.bwd_ws[k].data_ptr(), self.stream())
         return used
 
     def reduce_dw(self, k: int, n_slots: int, apply_sgd: bool = False) -> None:
@@ -486,9 +501,14 @@ class ProcState:
 # scatter
 
 
-def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, device=None) -> list:
+def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, device=None,
+            locality: bool = False) -> list:
     """Distribute row blocks per the partition and replicate the weights on the
-    device (runtime.py:233-275).  All ranks of this process share `device`."""
+    device (runtime.py:233-275).  All ranks of this process share `device`.
+
+    locality=True lays each rank's own rows out by label-propagation community
+    (locality.py) instead of ascending global id; `global_rows` then lists the
+    rows in that order (every host view follows it)."""
     h0 = dense(h0)
     if h0.shape != (a_hat.n_rows, model.dims[0]):
         raise ValueError(f"h0 has shape {h0.shape}, expected ({a_hat.n_rows}, {model.dims[0]})")
@@ -499,9 +519,14 @@ def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, 
         plan_bwd = build_comm_plan(a_bwd, pi, p)
     else:
         a_bwd, plan_bwd = a_hat, plan_fwd
+    labels = None
+    if locality:
+        from .locality import community_labels
+
+        labels = community_labels(a_hat)
     states = []
     for m in range(plan_fwd.p):
-        lay = build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, m)
+        lay = build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, m, row_labels=labels)
         states.append(ProcState(lay, plan_fwd, plan_bwd, model, h0[lay.global_rows], dev))
     return states
 

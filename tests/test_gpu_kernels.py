@@ -144,7 +144,7 @@ def test_dense_transform(d_in, d_out):
     close(devmem.download(yd, 3001, d_out), o.dmm(x, w))
 
 
-def _bwd(a, g, hp, w, act, with_gp, rows=None):
+def _bwd(a, g, hp, w, act, with_gp, rows=None, split=True):
     d = dev()
     d_k, d_p = g.shape[1], hp.shape[1]
     op = devmem.upload_csr(a, d)
@@ -154,10 +154,12 @@ def _bwd(a, g, hp, w, act, with_gp, rows=None):
     grid = _lib.bwd_grid(n, d_p, d_k, with_gp)
     part = torch.zeros((grid, d_p * devmem.ld_of(d_k)), dtype=torch.float32, device=d)
     rl = devmem.upload_index(rows, d) if rows is not None else None
+    ws_ld = _lib.bwd_workspace_ld(d_p, d_k) if split else 0
+    ws = torch.zeros((a.n_rows, ws_ld), dtype=torch.float32, device=d) if ws_ld else None
     _lib.call("gcnb_bwd_layer_f32", op.row_ptr.data_ptr(), op.col.data_ptr(), op.val.data_ptr(),
               0 if rl is None else rl.data_ptr(), n, gd.data_ptr(), gd.shape[1], d_k, hd.data_ptr(), hd.shape[1], d_p,
               wd.data_ptr(), 0 if gpd is None else gpd.data_ptr(), 0 if gpd is None else gpd.shape[1],
-              _lib.ACT[act], part.data_ptr(), devmem.stream_handle(None, d))
+              _lib.ACT[act], part.data_ptr(), 0 if ws is None else ws.data_ptr(), devmem.stream_handle(None, d))
     dw = torch.zeros((d_p, devmem.ld_of(d_k)), dtype=torch.float32, device=d)
     _lib.call("gcnb_reduce_partials_f32", part.data_ptr(), grid, dw.numel(), dw.data_ptr(), 0,
               devmem.stream_handle(None, d))
@@ -181,6 +183,19 @@ def test_bwd_layer(d_p, d_k, act):
     assert np.all(dwt[:, d_k:].cpu().numpy() == 0)
     _, dw_only, _ = _bwd(a, g, hp, w, act, False)
     close(dw_only, o.dmm_tn(hp, agg))
+
+
+@pytest.mark.parametrize("d_p,d_k", [(100, 128), (128, 47)])
+def test_bwd_split_equals_fused_bitwise(d_p, d_k):
+    """The two-kernel (workspace) form computes exactly the fused kernel's values."""
+    assert _lib.bwd_workspace_ld(d_p, d_k) > 0
+    a = rand_csr(2000, 2000, 0.005, 5)
+    rng = np.random.default_rng(1)
+    g, hp, w = rng.standard_normal((2000, d_k)), rng.standard_normal((2000, d_p)), rng.standard_normal((d_p, d_k))
+    rows = np.sort(rng.choice(2000, 1500, replace=False))
+    s = _bwd(a, g, hp, w, "relu", True, rows, split=True)
+    f = _bwd(a, g, hp, w, "relu", True, rows, split=False)
+    assert np.array_equal(s[0], f[0]) and np.array_equal(s[1], f[1])
 
 
 def test_bwd_layer_row_subsets_sum_to_full():

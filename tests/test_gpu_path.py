@@ -233,3 +233,25 @@ class TestRuntimeSemantics:
         assert [m.total_words for m in metrics] == words
         for w, wr in zip(states[0].weights, w_ref):
             close(w, wr)
+
+
+def test_locality_layout_same_results():
+    """Laying own rows out by community changes no result (layout only)."""
+    n, dims = 2000, (8, 12, 4)
+    raw = o.random_directed(n, 0.004, 9)
+    a_hat = gb.normalize_adjacency(gb.CsrMatrix(n, n, raw.row_offsets, raw.col_indices, raw.values))
+    h0 = np.random.default_rng(2).standard_normal((n, dims[0]))
+    ids, y = o.random_labels(n, dims[-1], 200, 9)
+    labels = gb.LabelSet(ids, y, dims[-1])
+    model = gb.init_model(dims, 9)
+    pi = gb.random_partition(a_hat.row_nnz(), gb.PartitionConfig(p=3, seed=9, epsilon=0.1))
+    runs = []
+    for loc in (False, True):
+        st = gb.scatter(a_hat, h0, pi, model, directed=True, locality=loc)
+        m = gb.train_epochs(st, gb.DeviceNetwork(3), labels, 2)
+        runs.append(([x.loss for x in m], st[0].weights, assemble(st, "h", 2), [x.total_words for x in m]))
+    close(runs[1][0], runs[0][0], 1e-6)
+    for a, b in zip(runs[1][1], runs[0][1]):
+        close(a, b, 1e-6)
+    close(runs[1][2], runs[0][2], 1e-6)
+    assert runs[0][3] == runs[1][3]

@@ -61,3 +61,27 @@ def test_hp_validation():
         hp.column_net_model(gb.CsrMatrix.from_coo(3, 3, [0], [1]))
     pi = hp.partition_hypergraph(a, 1)
     assert np.all(pi.assignment == 0)
+
+
+def test_label_propagation_recovers_blocks():
+    from paper_2212_05009_b200.locality import community_labels, rank_row_order
+
+    # two dense blocks joined by a single edge, randomly relabelled
+    n = 60
+    rng = np.random.default_rng(0)
+    rows, cols = [], []
+    for base in (0, 30):
+        for i in range(30):
+            for j in rng.choice(30, 8, replace=False):
+                if i != j:
+                    rows += [base + i, base + j]
+                    cols += [base + j, base + i]
+    rows += [0, 30]
+    cols += [30, 0]
+    perm = rng.permutation(n)
+    a = gb.normalize_adjacency(gb.CsrMatrix.from_coo(n, n, perm[rows], perm[cols], np.ones(len(rows))))
+    lab = community_labels(a)
+    blocks = [set(lab[perm[:30]]), set(lab[perm[30:]])]
+    assert len(blocks[0]) == 1 and len(blocks[1]) == 1 and blocks[0] != blocks[1]
+    order = rank_row_order(np.arange(n), lab)
+    assert sorted(order.tolist()) == list(range(n))
