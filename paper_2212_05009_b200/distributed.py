@@ -382,20 +382,24 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
     # rank 0 partitions (host preprocessing) and broadcasts the owner array
     box = [None]
     if rank == 0:
+        labels = None
+        if args.locality == "on" or args.partition == "hp-ml":
+            from .locality import community_labels
+
+            labels = community_labels(wl["a_hat"])
         if args.partition == "hp":
             from .hp import partition_hypergraph
 
             # reference defaults are 8 FM passes x 3 BFS restarts; 4 x 1 keeps
-            # a 0.4-2.4 M-vertex bisection tree within minutes
+            # a 0.4 M-vertex bisection tree within ~1-2 minutes
             pi = partition_hypergraph(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1)
+        elif args.partition == "hp-ml":
+            from .hp import partition_hypergraph_ml
+
+            pi = partition_hypergraph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, labels=labels)
         else:
             pi = random_partition(wl["a_hat"].row_nnz(), PartitionConfig(p=world, seed=args.seed, epsilon=0.01))
-        labels = None
-        if args.locality == "on":
-            from .locality import community_labels
-
-            labels = community_labels(wl["a_hat"])
-        box[0] = (pi.assignment, labels)
+        box[0] = (pi.assignment, labels if args.locality == "on" else None)
     dist.broadcast_object_list(box, src=0)
     owner = np.asarray(box[0][0], dtype=np.int64)
     row_labels = box[0][1]

@@ -205,7 +205,8 @@ def coarse_column_nets(model, labels: np.ndarray):
 
 
 def partition_hypergraph_ml(a_hat, p: int, seed: int = 0, epsilon: float = 0.01, sweeps: int = 5,
-                            fm_passes: int = 8, restarts: int = 3, directed: bool | None = None) -> Partition:
+                            fm_passes: int = 8, restarts: int = 3, directed: bool | None = None,
+                            labels: np.ndarray | None = None) -> Partition:
     """Two-level HP for 10^5-10^7-vertex inputs: label-propagation clusters
     (csrc_host/reorder.cpp) are the coarse vertices, the reference's recursive
     bisection + connectivity-1 FM partitions the contracted column-net
@@ -225,7 +226,7 @@ def partition_hypergraph_ml(a_hat, p: int, seed: int = 0, epsilon: float = 0.01,
     weights = np.asarray(model.row_nnz(), dtype=np.int64)
     if p == 1:
         return Partition.from_assignment(np.zeros(a_hat.n_rows, dtype=np.int64), weights, 1, epsilon)
-    lab = community_labels(model, sweeps=sweeps)
+    lab = community_labels(model, sweeps=sweeps) if labels is None else np.asarray(labels)
     _, lab = np.unique(lab, return_inverse=True)
     coarse = coarse_column_nets(model, lab)
     cfg = PartitionConfig(p=p, epsilon=epsilon, seed=seed, fm_passes=fm_passes, restarts=restarts)

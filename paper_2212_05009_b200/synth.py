@@ -18,8 +18,11 @@ is deterministic in `seed` and documented in BASELINE.md §4 / DESIGN.md §6.
 * roadnet  — undirected 1404×1404 lattice (1,971,216 vertices) keeping exactly
              2,766,607 of its edges (5,533,214 stored nonzeros), relabelled.
 * products — undirected degree-corrected SBM, 2,449,029 vertices, exactly
-             61,859,140 pairs (123,718,280 stored nonzeros), 2,048 blocks,
-             80 % intra-block pairs, log-normal degree propensities, relabelled.
+             61,859,140 pairs (123,718,280 stored nonzeros), 2,048 blocks on a
+             ring, 80 % intra-block pairs, the rest to a block at a two-sided
+             geometric ring offset (mean 16 blocks: related categories),
+             log-normal degree propensities, relabelled.  (Uniform inter-block
+             partners made the graph an expander: HP/RP halo ratio 0.63 at p=8.)
 """
 
 from __future__ import annotations
@@ -102,7 +105,7 @@ def roadnet(seed: int = 0, side: int = 1404, kept_edges: int = 2_766_607) -> Csr
 
 
 def products(seed: int = 0, n: int = 2_449_029, pairs: int = 61_859_140, blocks: int = 2048,
-             intra: float = 0.8, sigma: float = 1.0) -> CsrMatrix:
+             intra: float = 0.8, sigma: float = 1.0, block_offset: float = 16.0) -> CsrMatrix:
     rng = np.random.default_rng([seed, 0x9200])
     block = np.sort(rng.integers(0, blocks, n))          # contiguous blocks before relabelling
     bounds = np.searchsorted(block, np.arange(blocks + 1))
@@ -119,14 +122,16 @@ def products(seed: int = 0, n: int = 2_449_029, pairs: int = 61_859_140, blocks:
     def draw(k):
         u = inv_cdf(rng.random(k) * cum[-1])
         same = rng.random(k) < intra
-        # intra-block partner: inverse-CDF draw restricted to u's block
-        lo = bounds[block[u]]
-        hi = bounds[block[u] + 1]
+        # partner block: u's own block (intra) or a block at a two-sided
+        # geometric offset on the block ring (related categories); partner ∝
+        # propensity inside that block (inverse CDF restricted to the block)
+        off = rng.geometric(1.0 / block_offset, k) * np.where(rng.random(k) < 0.5, -1, 1)
+        b = np.where(same, block[u], (block[u] + off) % blocks)
+        lo = bounds[b]
+        hi = np.maximum(bounds[b + 1], lo + 1)
         c_lo = np.where(lo > 0, cum[np.maximum(lo - 1, 0)], 0.0)
-        c_hi = cum[hi - 1]
-        w_in = inv_cdf(c_lo + rng.random(k) * (c_hi - c_lo))
-        w_any = inv_cdf(rng.random(k) * cum[-1])
-        w = np.where(same, w_in, w_any)
+        c_hi = cum[np.minimum(hi, n) - 1]
+        w = inv_cdf(c_lo + rng.random(k) * (c_hi - c_lo))
         keep = u != w
         a, b = np.minimum(u[keep], w[keep]), np.maximum(u[keep], w[keep])
         return _uniq(a * n + b)
