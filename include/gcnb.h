@@ -121,11 +121,12 @@ int gcnb_fwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* 
                        const float* w, int32_t d_out,
                        float* h, int32_t ldh, int32_t act, void* stream);
 
-/* Dense transform Y = X·W for n_rows contiguous rows (the `@ w` of
- * runtime.py:299/304 hoisted before aggregation when d_out < d_in). */
-int gcnb_dense_f32(const float* x, int32_t ldx, int32_t n_rows, int32_t d_in,
-                   const float* w, int32_t d_out, float* y, int32_t ldy,
-                   void* stream);
+/* Dense transform Y[r] = act(X[r]·W) for r = rows[i] (rows == NULL: r = i),
+ * i < n_rows: the `@ w` of runtime.py:299/304 hoisted before aggregation when
+ * d_out < d_in, or the second half of a split aggregate-then-transform layer. */
+int gcnb_dense_f32(const float* x, int32_t ldx, const int32_t* rows, int32_t n_rows,
+                   int32_t d_in, const float* w, int32_t d_out, float* y, int32_t ldy,
+                   int32_t act, void* stream);
 
 /* runtime._bwd_compute (runtime.py:344-356) for the row list `rows`:
  *   agg[r]   = A_back[r,:]·G                       (G extended, d_k wide)

@@ -219,6 +219,8 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
 // ---------------------------------------------------------------------------
 // Tile GEMM: acc[u] (tile rows trg + u*RG, cols 4tc..4tc+3) = Σ_k Ys[r][k]·Ws[k][4tc..]
 template <int RPT>
+// (Reading Y four k at a time measured no faster on products and raised
+// register counts of the RPT = 8 variants; kept as one k per step.)
 __device__ __forceinline__ void tile_gemm(const float* __restrict__ Ys, int ys_ld, const float* __restrict__ Ws,
                                           int ws_ld, int K, int trg, int RG, int tc, int rpt, float4 (&acc)[RPT]) {
 #pragma unroll
@@ -299,13 +301,14 @@ __global__ void __launch_bounds__(NT) k_fwd_gemm(const int* __restrict__ rp, con
   const int ld_in = (d_in + 3) & ~3;
   const int ld_out = (d_out + 3) & ~3;
   const int ys_ld = ld_in + 4;
-  const int w_floats = W ? d_in * ld_out : 0;
-  float* Ws = smem;                     // d_in × ld_out
+  const int w_floats = W ? ld_in * ld_out : 0;
+  float* Ws = smem;                     // ld_in × ld_out (rows >= d_in zero)
   float* Ys = smem + w_floats;          // T × ys_ld
   if (W) {
     const float4* W4 = reinterpret_cast<const float4*>(W);
     float4* Ws4 = reinterpret_cast<float4*>(Ws);
-    for (int idx = threadIdx.x; idx < d_in * ld_out / 4; idx += NT) Ws4[idx] = __ldg(W4 + idx);
+    for (int idx = threadIdx.x; idx < ld_in * ld_out / 4; idx += NT)
+      Ws4[idx] = idx < d_in * ld_out / 4 ? __ldg(W4 + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int c4o = ld_out / 4;
   const int RG = NT / c4o;
@@ -362,13 +365,13 @@ __global__ void __launch_bounds__(NT) k_bwd(const int* __restrict__ rp, const in
   const int ld_p = (d_prev + 3) & ~3;
   const int as_ld = ld_k + 4;
   const int hs_ld = ld_p + 4;
-  float* Wts = smem;                              // d_k × ld_p  (Wᵀ), GP only
-  float* As = smem + (GP ? d_k * ld_p : 0);       // T × as_ld
+  float* Wts = smem;                              // ld_k × ld_p  (Wᵀ, pad rows/cols zero), GP only
+  float* As = smem + (GP ? ld_k * ld_p : 0);      // T × as_ld
   float* Hs = As + T * as_ld;                     // T × hs_ld
   if (GP) {
-    for (int idx = threadIdx.x; idx < d_k * ld_p; idx += NT) {
+    for (int idx = threadIdx.x; idx < ld_k * ld_p; idx += NT) {
       const int c = idx / ld_p, i = idx - c * ld_p;
-      Wts[idx] = i < d_prev ? __ldg(W + (size_t)i * ld_k + c) : 0.0f;
+      Wts[idx] = (i < d_prev && c < d_k) ? __ldg(W + (size_t)i * ld_k + c) : 0.0f;
     }
   }
   const int c4k = ld_k / 4, c4p = ld_p / 4;
@@ -651,7 +654,7 @@ int bwd_plan(int n_rows, int d_prev, int d_k, bool with_gp, BwdPlan* out) {
   else if (ipt <= 16) fn = pick_bwd_ipt<16>(s, with_gp, rpt);
   else if (ipt <= 32) fn = pick_bwd_ipt<32>(s, with_gp, rpt);
   GCNB_REQUIRE(fn != nullptr, "bwd layer: unsupported widths d_prev=%d d_k=%d", d_prev, d_k);
-  const size_t smem = sizeof(float) * ((with_gp ? (size_t)d_k * ld_p : 0) + (size_t)T * (ld_k + 4) +
+  const size_t smem = sizeof(float) * ((with_gp ? (size_t)ld_k * ld_p : 0) + (size_t)T * (ld_k + 4) +
                                        (size_t)T * (ld_p + 4) + 4 * NT);
   GCNB_REQUIRE(smem <= 227 * 1024, "bwd layer: tile does not fit shared memory (d_prev=%d d_k=%d)", d_prev, d_k);
   const int n_tiles = std::max(1, (n_rows + T - 1) / T);
@@ -698,7 +701,8 @@ int launch_fwd_gemm(bool agg, const int32_t* row_ptr, const int32_t* col, const 
   const int T = tile_rows(d_out, s.lpr, &rpt);
   FwdFn fn = agg ? pick_fwd<true>(s, rpt) : pick_fwd<false>(s, rpt);
   GCNB_REQUIRE(fn != nullptr, "%s: unsupported width %d", what, d_in);
-  const size_t smem = sizeof(float) * ((w ? (size_t)d_in * round4(d_out) : 0) + (size_t)T * (round4(d_in) + 4));
+  const size_t smem =
+      sizeof(float) * ((w ? (size_t)round4(d_in) * round4(d_out) : 0) + (size_t)T * (round4(d_in) + 4));
   GCNB_REQUIRE(smem <= 227 * 1024, "%s: tile does not fit shared memory", what);
   const int grid = occupancy_grid(reinterpret_cast<const void*>(fn), smem, (n_rows + T - 1) / T);
   fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, x, ldx, d_in, w, d_out, h, ldh, act, T);
@@ -742,16 +746,17 @@ extern "C" int gcnb_fwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
                          "fwd layer (aggregate+transform)");
 }
 
-extern "C" int gcnb_dense_f32(const float* x, int32_t ldx, int32_t n_rows, int32_t d_in, const float* w,
-                              int32_t d_out, float* y, int32_t ldy, void* stream) {
+extern "C" int gcnb_dense_f32(const float* x, int32_t ldx, const int32_t* rows, int32_t n_rows, int32_t d_in,
+                              const float* w, int32_t d_out, float* y, int32_t ldy, int32_t act, void* stream) {
   GCNB_REQUIRE(n_rows >= 0, "dense: n_rows must be >= 0");
+  GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "dense: unknown activation %d", act);
   GCNB_REQUIRE(d_in >= 1 && d_in <= 256 && d_out >= 1 && d_out <= 256, "dense: widths out of range");
   GCNB_REQUIRE(ldx % 4 == 0 && ldy % 4 == 0 && ldx >= round4(d_in) && ldy >= round4(d_out),
                "dense: row strides must be multiples of 4 and cover the widths");
   GCNB_REQUIRE(x && w && y && aligned16(x) && aligned16(w) && aligned16(y), "dense: operands must be 16-byte aligned");
   if (n_rows == 0) return GCNB_OK;
-  return launch_fwd_gemm(false, nullptr, nullptr, nullptr, nullptr, n_rows, x, ldx, d_in, w, d_out, y, ldy,
-                         GCNB_ACT_IDENTITY, (cudaStream_t)stream, "dense");
+  return launch_fwd_gemm(false, nullptr, nullptr, nullptr, rows, n_rows, x, ldx, d_in, w, d_out, y, ldy, act,
+                         (cudaStream_t)stream, "dense");
 }
 
 extern "C" int gcnb_bwd_grid(int32_t n_rows, int32_t d_prev, int32_t d_k, int32_t with_gprev, int32_t* grid_out) {

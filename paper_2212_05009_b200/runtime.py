@@ -279,6 +279,13 @@ class ProcState:
                 slots = max(gi + gb, ga)
                 self.partials[k] = torch.zeros((slots, self.dims[k - 1] * devmem.ld_of(self.dims[k])),
                                                dtype=torch.float32, device=dev)
+            # forward: wide aggregate-first layers (d_in·d_out > 2048) run as
+            # aggregation + dense transform through a Y workspace
+            self.fwd_ws = [None] * (L + 1)
+            for k in range(1, L + 1):
+                if not self.transform_first[k] and self.dims[k - 1] * devmem.ld_of(self.dims[k]) > 2048:
+                    self.fwd_ws[k] = torch.zeros((max(n, 1), devmem.ld_of(self.dims[k - 1])), dtype=torch.float32,
+                                                 device=dev)
             # split-mode workspace (agg rows) for large-ΔW layers (gcnb_bwd_workspace_ld)
             self.bwd_ws = [None] * (L + 1)
             for k in range(1, L + 1):
@@ -392,8 +399,8 @@ class ProcState:
         x = self.hbuf[k - 1]
         n, a, b = self.n_own, self.dims[k - 1], self.dims[k]
         with span(f"dense{k}", 4 * (n * a + a * b + n * b), 2 * n * a * b, self.stream()):
-            _lib.call("gcnb_dense_f32", x.data_ptr(), x.shape[1], n, a, self.w[k].data_ptr(), b,
-                      self.xext[k].data_ptr(), self.xext[k].shape[1], self.stream())
+            _lib.call("gcnb_dense_f32", x.data_ptr(), x.shape[1], None, n, a, self.w[k].data_ptr(), b,
+                      self.xext[k].data_ptr(), self.xext[k].shape[1], _lib.ACT["identity"], self.stream())
 
     def fwd_compute(self, k: int, rows: str = "all") -> None:
         """runtime._fwd_compute for the selected own rows (all | interior | boundary)."""
@@ -407,6 +414,20 @@ class ProcState:
         w = self.w[k].data_ptr() if fused else 0
         nnz = op.nnz_of(rows)
         d_out = self.dims[k]
+        if fused and self.fwd_ws[k] is not None:
+            # wide layer: the gather-bound aggregation runs alone at full
+            # occupancy (Y → workspace), then the dense transform streams Y
+            ws = self.fwd_ws[k]
+            with span(f"fwd{k}", 4 * (n_sel + 1) + 8 * nnz + 4 * width * nnz + 4 * width * n_sel, 2 * nnz * width,
+                      self.stream()):
+                _lib.call("gcnb_fwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
+                          op.csr.val.data_ptr(), sel, n_sel, x.data_ptr(), x.shape[1], width, 0, width,
+                          ws.data_ptr(), ws.shape[1], _lib.ACT["identity"], self.stream())
+            with span(f"dense{k}", 4 * (n_sel * width + width * d_out + n_sel * d_out),
+                      2 * n_sel * width * d_out, self.stream()):
+                _lib.call("gcnb_dense_f32", ws.data_ptr(), ws.shape[1], sel, n_sel, width, w, d_out, h.data_ptr(),
+                          h.shape[1], self.act, self.stream())
+            return
         algo = 4 * (n_sel + 1) + 8 * nnz + 4 * width * nnz + 4 * d_out * n_sel
         flops = 2 * nnz * width
         if fused:

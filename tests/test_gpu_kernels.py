@@ -139,9 +139,17 @@ def test_dense_transform(d_in, d_out):
     d = dev()
     xd, wd = devmem.upload_dense(x, d), devmem.upload_dense(w, d)
     yd = devmem.empty_rows(3001, d_out, d)
-    _lib.call("gcnb_dense_f32", xd.data_ptr(), xd.shape[1], 3001, d_in, wd.data_ptr(), d_out, yd.data_ptr(),
-              yd.shape[1], devmem.stream_handle(None, d))
+    _lib.call("gcnb_dense_f32", xd.data_ptr(), xd.shape[1], None, 3001, d_in, wd.data_ptr(), d_out, yd.data_ptr(),
+              yd.shape[1], _lib.ACT["identity"], devmem.stream_handle(None, d))
     close(devmem.download(yd, 3001, d_out), o.dmm(x, w))
+    # row list + ReLU: only the listed rows are written
+    rows = np.arange(0, 3001, 3)
+    yd2 = devmem.empty_rows(3001, d_out, d)
+    _lib.call("gcnb_dense_f32", xd.data_ptr(), xd.shape[1], devmem.upload_index(rows, d).data_ptr(), len(rows), d_in,
+              wd.data_ptr(), d_out, yd2.data_ptr(), yd2.shape[1], _lib.ACT["relu"], devmem.stream_handle(None, d))
+    got = devmem.download(yd2, 3001, d_out)
+    close(got[rows], np.maximum(o.dmm(x, w)[rows], 0))
+    assert np.all(got[np.setdiff1d(np.arange(3001), rows)] == 0)
 
 
 def _bwd(a, g, hp, w, act, with_gp, rows=None, split=True):
