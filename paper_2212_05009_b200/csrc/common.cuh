@@ -23,6 +23,11 @@ int set_error(int code, const char* fmt, ...);
 int cuda_fail(cudaError_t e, const char* what);
 int num_sms();
 
+// dense.cu: register-blocked SIMT transform for the wide dense layers
+bool dense_blocked_applies(int d_in, int d_out);
+int launch_dense_blocked(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
+                         float* y, int ldy, int act, cudaStream_t st);
+
 // After every <<<>>> launch: surface launch errors, count the launch.
 #define GCNB_AFTER_LAUNCH(what)                                         \
   do {                                                                  \

@@ -755,6 +755,8 @@ extern "C" int gcnb_dense_f32(const float* x, int32_t ldx, const int32_t* rows, 
                "dense: row strides must be multiples of 4 and cover the widths");
   GCNB_REQUIRE(x && w && y && aligned16(x) && aligned16(w) && aligned16(y), "dense: operands must be 16-byte aligned");
   if (n_rows == 0) return GCNB_OK;
+  if (dense_blocked_applies(d_in, d_out))
+    return launch_dense_blocked(x, ldx, rows, n_rows, d_in, w, d_out, y, ldy, act, (cudaStream_t)stream);
   return launch_fwd_gemm(false, nullptr, nullptr, nullptr, rows, n_rows, x, ldx, d_in, w, d_out, y, ldy, act,
                          (cudaStream_t)stream, "dense");
 }

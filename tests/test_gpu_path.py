@@ -255,3 +255,25 @@ def test_locality_layout_same_results():
         close(a, b, 1e-6)
     close(runs[1][2], runs[0][2], 1e-6)
     assert runs[0][3] == runs[1][3]
+
+
+@pytest.mark.parametrize("directed", [False, True])
+def test_wide_layers_split_paths_against_oracle(directed):
+    """Wide layers (d_in·d_out > 2048) take the split forward (aggregation + dense
+    transform) and split backward (aggregation + dense epilogue) paths."""
+    n, dims = 3000, (64, 96, 40)
+    raw = o.random_directed(n, 0.003, 4) if directed else o.random_undirected(n, 0.003, 4)
+    a_hat = gb.normalize_adjacency(gb.CsrMatrix(n, n, raw.row_offsets, raw.col_indices, raw.values))
+    h0 = np.random.default_rng(5).standard_normal((n, dims[0]))
+    ids, y = o.random_labels(n, dims[-1], 300, 4)
+    model = gb.init_model(dims, 4)
+    pi = gb.random_partition(a_hat.row_nnz(), gb.PartitionConfig(p=2, seed=4, epsilon=0.1))
+    states = gb.scatter(a_hat, h0, pi, model, directed=directed, locality=True)
+    assert states[0].fwd_ws[1] is not None and states[0].bwd_ws[1] is not None and states[0].bwd_ws[2] is not None
+    metrics = gb.train_epochs(states, gb.DeviceNetwork(2), gb.LabelSet(ids, y, dims[-1]), 2)
+    w_ref, losses, words, _ = o.parallel_train(o.as_csr(a_hat), h0, pi.assignment, 2, list(model.weights), ids, y,
+                                               2, directed=directed)
+    close([m.loss for m in metrics], losses)
+    assert [m.total_words for m in metrics] == words
+    for w, wr in zip(states[1].weights, w_ref):
+        close(w, wr)
