@@ -1,4 +1,4 @@
-"""Hypergraph (HP) partitioning: recursive bisection with connectivity-1 FM.
+"""HP / GP / SHP partitioning: recursive bisection with FM refinement.
 
 Restates the reference partitioner (gcnpart partition.py:486-559,
 `partition_hypergraph_fm` / `_partition_by_bisection` / `_recursive_bisect`)
@@ -12,7 +12,9 @@ reference, so small instances give the reference's assignment bit-exactly
 The column-net model of Â (net j = rows with a nonzero in column j, unit
 cost, vertex weight = row nnz; models.py:175-186) is built as the pattern of
 Âᵀ; directed inputs are partitioned on the symmetrised pattern as the
-reference's CLI does (cli.py:162-176, 225).
+reference's CLI does (cli.py:162-176, 225).  GP (partition_graph_fm, tag
+0x4750) runs the same engine on 2-pin nets, one per undirected edge; SHP
+(partition_stochastic) runs HP on the merged column nets of b sampled batches.
 """
 
 from __future__ import annotations
@@ -163,6 +165,72 @@ def partition_hypergraph_fm(h, cfg: PartitionConfig) -> Partition:
     """HP on a hypergraph (NetList or gcnpart Hypergraph) — partition.py:544-559."""
     if not isinstance(h, NetList):
         h = NetList.from_hypergraph(h)
+    return _partition_by_bisection(h, cfg, 0x4850)
+
+
+def graph_net_list(a) -> NetList:
+    """GP's graph model (models.py:158-172) as 2-pin nets: the symmetrised
+    off-diagonal pattern as unique (u < v) pairs in lexicographic order, unit
+    costs, w(v) = row nnz.  For 2-pin nets the connectivity-1 cut and every FM
+    gain equal the edge cut and GraphBisection's gains (partition.py:60-117),
+    and integer costs keep the incremental updates exact, so the shared
+    bisection engine reproduces partition_graph_fm move for move."""
+    if a.n_rows != a.n_cols:
+        raise ValueError("matrix must be square")
+    ro = np.asarray(a.row_offsets, dtype=np.int64)
+    ci = np.asarray(a.col_indices, dtype=np.int64)
+    n = a.n_rows
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))
+    off = rows != ci
+    u, v = np.minimum(rows[off], ci[off]), np.maximum(rows[off], ci[off])
+    key = np.unique(u * n + v)
+    pins = np.stack([key // n, key % n], axis=1).reshape(-1)
+    ptr = np.arange(0, 2 * len(key) + 1, 2, dtype=np.int64)
+    return NetList(n, ptr, pins, None, np.diff(ro))
+
+
+def partition_graph_fm(g, cfg: PartitionConfig) -> Partition:
+    """GP: recursive bisection with edge-cut FM (partition.py:526-541), on a
+    graph_net_list (or a gcnpart UGraph)."""
+    if not isinstance(g, NetList):
+        e = np.asarray(g.edges, dtype=np.int64).reshape(-1, 2)
+        cost = np.asarray(g.edge_cost, dtype=np.float64)
+        if np.any(cost != np.round(cost)):
+            raise ValueError("GP engine needs integer edge costs")
+        g = NetList(g.n_vertices, np.arange(0, 2 * len(e) + 1, 2), e.reshape(-1), cost.astype(np.int64),
+                    g.vertex_weight)
+    return _partition_by_bisection(g, cfg, 0x4750)
+
+
+def stochastic_net_list(a, batch_size: int, b: int, seed: int) -> NetList:
+    """SHP's merged hypergraph (models.py:279-291): the column nets of each of
+    b sampled batches' induced patterns (with self loops), pins mapped back to
+    global ids, concatenated batch by batch; full-graph vertex weights."""
+    from .host import MiniBatchSpec, induced_pattern, sample_batches
+
+    if a.n_rows != a.n_cols:
+        raise ValueError("matrix must be square")
+    ptrs, pins = [np.zeros(1, dtype=np.int64)], []
+    base = 0
+    for batch in sample_batches(a.n_rows, MiniBatchSpec(batch_size), b, seed):
+        sub = column_net_model(induced_pattern(a, batch))
+        pins.append(batch[sub.pins])
+        ptrs.append(sub.ptr[1:] + base)
+        base += len(sub.pins)
+    return NetList(a.n_rows, np.concatenate(ptrs), np.concatenate(pins), None,
+                   np.diff(np.asarray(a.row_offsets, dtype=np.int64)))
+
+
+def partition_stochastic(a, batch_size: int, b: int, cfg: PartitionConfig) -> Partition:
+    """SHP (partition.py:562-575): HP of the merged hypergraph of b sampled
+    batches; vertices no batch sampled carry no nets and are placed by weight."""
+    if b < 1:
+        raise ValueError("stochastic partitioning needs at least one batch")
+    return partition_hypergraph_fm(stochastic_net_list(a, batch_size, b, cfg.seed), cfg)
+
+
+def _partition_by_bisection(h: NetList, cfg: PartitionConfig, tag: int) -> Partition:
+    """partition.py:503-523 over the shared C++ bisection engine."""
     n = h.n
     weights = np.asarray(h.vertex_weight, dtype=np.int64)
     if cfg.p > n:
@@ -173,7 +241,7 @@ def partition_hypergraph_fm(h, cfg: PartitionConfig) -> Partition:
         raise ValueError(f"internal partitioners use recursive bisection and need p to be a power of two "
                          f"(got {cfg.p}); use an external partition file for other p")
     cap_leaf = (1.0 + cfg.epsilon) * float(weights.sum()) / cfg.p
-    rng = np.random.default_rng([int(cfg.seed), 0x4850])
+    rng = np.random.default_rng([int(cfg.seed), tag])
     assignment = np.full(n, -1, dtype=np.int64)
     _recursive_bisect(h, np.arange(n, dtype=np.int64), cfg.p, 0, assignment, weights, cap_leaf, rng, cfg)
     pi = Partition.from_assignment(assignment, weights, cfg.p, cfg.epsilon)

@@ -218,8 +218,37 @@ def partitions(g, helpers):
     np.savez_compressed(OUT / "partitions.npz", **out)
 
 
+def partitions_gp_shp(g, helpers):
+    """GP (partition_graph_fm, partition.py:526-541) and SHP (partition_stochastic,
+    partition.py:562-575) assignments of gcnpart itself on small seeded instances."""
+    from gcnpart import cli
+
+    out = {}
+    cases = [(40, 0.1, 1, 2, 0.05), (120, 0.04, 3, 8, 0.05), (300, 0.02, 4, 4, 0.03), (500, 0.01, 5, 8, 0.05)]
+    for i, (n, dens, seed, p, eps) in enumerate(cases):
+        raw = helpers.random_undirected(n, dens, seed)
+        a = g.normalize_adjacency(raw)
+        cfg = g.PartitionConfig(p=p, seed=seed, epsilon=eps)
+        out[f"c{i}_case"] = np.array([n, p, seed], dtype=np.float64)
+        out[f"c{i}_dens_eps"] = np.array([dens, eps])
+        out[f"c{i}_gp"] = g.partition_graph_fm(g.build_graph_model(a), cfg).assignment
+        bs, b = max(n // 4, p), 3
+        out[f"c{i}_shp_bs_b"] = np.array([bs, b])
+        out[f"c{i}_shp"] = g.partition_stochastic(a, g.MiniBatchSpec(bs), b, cfg).assignment
+    raw = helpers.random_directed(200, 0.02, 9)
+    a = cli._symmetrized(g.normalize_adjacency(raw))
+    cfg = g.PartitionConfig(p=4, seed=9, epsilon=0.05)
+    out["dir_gp"] = g.partition_graph_fm(g.build_graph_model(a), cfg).assignment
+    out["dir_shp"] = g.partition_stochastic(a, g.MiniBatchSpec(60), 4, cfg).assignment
+    np.savez_compressed(OUT / "partitions_gp_shp.npz", **out)
+
+
 def main():
     g, helpers = _import_reference()
+    if "--only-gp-shp" in sys.argv:
+        partitions_gp_shp(g, helpers)
+        return
+    partitions_gp_shp(g, helpers)
     partitions(g, helpers)
     kat(g, helpers)
     small_instances(g, helpers)

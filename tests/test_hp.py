@@ -35,6 +35,30 @@ def test_hp_directed_uses_symmetrised_model():
     assert np.array_equal(pi.assignment, z["dir_assign"])
 
 
+@pytest.mark.parametrize("i", range(4))
+def test_gp_and_shp_match_reference_assignment(i):
+    """GP (partition_graph_fm) and SHP (partition_stochastic) against gcnpart's own
+    assignments (tests/golden/partitions_gp_shp.npz)."""
+    z = load("partitions_gp_shp")
+    n, p, seed = (int(x) for x in z[f"c{i}_case"])
+    dens, eps = z[f"c{i}_dens_eps"]
+    a = _a_hat(o.random_undirected(n, float(dens), seed))
+    cfg = gb.PartitionConfig(p=p, seed=seed, epsilon=float(eps))
+    gp = hp.partition_graph_fm(hp.graph_net_list(a), cfg)
+    assert np.array_equal(gp.assignment, z[f"c{i}_gp"]) and gp.is_balanced()
+    bs, b = (int(x) for x in z[f"c{i}_shp_bs_b"])
+    shp = hp.partition_stochastic(a, bs, b, cfg)
+    assert np.array_equal(shp.assignment, z[f"c{i}_shp"]) and shp.is_balanced()
+
+
+def test_gp_shp_directed_on_symmetrised_pattern():
+    z = load("partitions_gp_shp")
+    a = hp.symmetrized(_a_hat(o.random_directed(200, 0.02, 9)))
+    cfg = gb.PartitionConfig(p=4, seed=9, epsilon=0.05)
+    assert np.array_equal(hp.partition_graph_fm(hp.graph_net_list(a), cfg).assignment, z["dir_gp"])
+    assert np.array_equal(hp.partition_stochastic(a, 60, 4, cfg).assignment, z["dir_shp"])
+
+
 def test_hp_cut_equals_plan_volume_and_beats_rp():
     # locality graph: a 30x30 grid, randomly relabelled
     side = 30
