@@ -44,9 +44,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="amazon0601")
-    ap.add_argument("--partition", default="hp-ml", choices=("rp", "hp", "hp-ml"),
+    ap.add_argument("--partition", default="hp-ml", choices=("rp", "hp", "hp-ml", "gp", "gp-ml"),
                     help="row partition for N>1 (BASELINE config[1] names HP): hp = the reference's flat "
-                         "recursive-bisection FM (C++), hp-ml = the same FM on label-propagation clusters")
+                         "recursive-bisection FM (C++), hp-ml = the same FM on label-propagation clusters; "
+                         "gp / gp-ml = the edge-cut (graph model) twins (BASELINE config[2] compares HP/GP/RP)")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--seed", type=int, default=0)

@@ -109,10 +109,16 @@ __device__ __forceinline__ void aggregate_span(const int* __restrict__ col, cons
 // copies are memory operations the scheduler cannot sink next to their uses,
 // so U gathers per lane are genuinely in flight, at no register cost.  Each
 // lane reads back only the slot it filled itself (no warp barrier needed).
+// Predicated off (not zero-filled) when !pred: a src-size-0 copy still sends
+// its sector request through L1/L2 (ncu measured 1.5x the algorithmic gather
+// bytes on products from the idle chunk lanes), a predicated one does not.
+// The slot then holds stale data, so callers must not consume it.
 __device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src, bool pred) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-  const int sz = pred ? 16 : 0;  // src-size 0: zero-fill, no global access
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem_src), "r"(sz) : "memory");
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q cp.async.cg.shared.global [%0], [%1], 16;\n\t}" ::"r"(s), "l"(gmem_src), "r"((int)pred)
+      : "memory");
 }
 
 template <int LPR, int VPL, int U>
@@ -137,25 +143,28 @@ __device__ __forceinline__ void aggregate_span_cp(const int* __restrict__ col, c
     const int cnt = min(LPR, maxlen - base);
     for (int t0 = 0; t0 < cnt; t0 += U) {
       float vv[U];
+      bool okv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int t = t0 + u;
         const int c = __shfl_sync(0xffffffffu, cj, t & (LPR - 1), LPR);
         const float v = __shfl_sync(0xffffffffu, vj, t & (LPR - 1), LPR);
-        const bool ok = t < cnt && base + t < len;
-        vv[u] = ok ? v : 0.0f;
-        const float4* xr = X4 + (size_t)(ok ? c : 0) * ldx4;
+        okv[u] = t < cnt && base + t < len;
+        vv[u] = v;
+        const float4* xr = X4 + (size_t)c * ldx4;
 #pragma unroll
         for (int q = 0; q < VPL; ++q) {
           const int ch = gl + q * LPR;
-          cp_async_16(stage + (u * VPL + q) * 32 + lane, xr + ch, ok && ch < c4);
+          cp_async_16(stage + (u * VPL + q) * 32 + lane, xr + ch, okv[u] && ch < c4);
         }
       }
       asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+      // chunks past c4 are never stored by the caller, so only okv gates
 #pragma unroll
       for (int u = 0; u < U; ++u) {
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) acc[q] = fma4(vv[u], stage[(u * VPL + q) * 32 + lane], acc[q]);
+        for (int q = 0; q < VPL; ++q)
+          if (okv[u]) acc[q] = fma4(vv[u], stage[(u * VPL + q) * 32 + lane], acc[q]);
       }
     }
     cj = cn;

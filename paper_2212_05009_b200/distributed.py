@@ -383,7 +383,7 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
     box = [None]
     if rank == 0:
         labels = None
-        if args.locality == "on" or args.partition == "hp-ml":
+        if args.locality == "on" or args.partition.endswith("-ml"):
             from .locality import community_labels
 
             labels = community_labels(wl["a_hat"])
@@ -397,6 +397,14 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
             from .hp import partition_hypergraph_ml
 
             pi = partition_hypergraph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, labels=labels)
+        elif args.partition == "gp":
+            from .hp import partition_graph
+
+            pi = partition_graph(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1)
+        elif args.partition == "gp-ml":
+            from .hp import partition_graph_ml
+
+            pi = partition_graph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, labels=labels)
         else:
             pi = random_partition(wl["a_hat"].row_nnz(), PartitionConfig(p=world, seed=args.seed, epsilon=0.01))
         box[0] = (pi.assignment, labels if args.locality == "on" else None)

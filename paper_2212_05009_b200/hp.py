@@ -272,6 +272,29 @@ def coarse_column_nets(model, labels: np.ndarray):
     return NetList(C, ptr, cl, None, w)
 
 
+def coarse_graph_nets(model, labels: np.ndarray) -> NetList:
+    """GP's graph model of `model` contracted onto clusters `labels` (0..C-1):
+    one 2-pin net per pair of adjacent clusters with cost = the number of fine
+    edges between them, so the coarse edge cut equals the projected fine cut."""
+    g = graph_net_list(model)
+    C = int(labels.max()) + 1
+    cu, cv = labels[g.pins[0::2]], labels[g.pins[1::2]]
+    keep = cu != cv
+    lo, hi = np.minimum(cu[keep], cv[keep]), np.maximum(cu[keep], cv[keep])
+    key, cnt = np.unique(lo * C + hi, return_counts=True)
+    pins = np.stack([key // C, key % C], axis=1).reshape(-1)
+    w = np.bincount(labels, weights=np.asarray(model.row_nnz(), dtype=np.float64), minlength=C).astype(np.int64)
+    return NetList(C, np.arange(0, 2 * len(key) + 1, 2), pins, cnt, w)
+
+
+def partition_graph_ml(a_hat, p: int, seed: int = 0, epsilon: float = 0.01, sweeps: int = 5, fm_passes: int = 8,
+                       restarts: int = 3, directed: bool | None = None, labels: np.ndarray | None = None) -> Partition:
+    """Two-level GP (label-propagation clusters → edge-cut FM on the contracted
+    graph, rng tag 0x4750 → projection + k-way repair), the graph-model twin of
+    partition_hypergraph_ml."""
+    return _partition_ml(a_hat, p, seed, epsilon, sweeps, fm_passes, restarts, directed, labels, "gp")
+
+
 def partition_hypergraph_ml(a_hat, p: int, seed: int = 0, epsilon: float = 0.01, sweeps: int = 5,
                             fm_passes: int = 8, restarts: int = 3, directed: bool | None = None,
                             labels: np.ndarray | None = None) -> Partition:
@@ -282,6 +305,10 @@ def partition_hypergraph_ml(a_hat, p: int, seed: int = 0, epsilon: float = 0.01,
     k-way weight repair if the projection misses the balance cap.  (The
     reference's flat FM is O(n) per move; PaToH, which the paper used, is
     multilevel in the same spirit.)"""
+    return _partition_ml(a_hat, p, seed, epsilon, sweeps, fm_passes, restarts, directed, labels, "hp")
+
+
+def _partition_ml(a_hat, p, seed, epsilon, sweeps, fm_passes, restarts, directed, labels, kind) -> Partition:
     from .locality import community_labels
 
     if directed is None:
@@ -296,9 +323,15 @@ def partition_hypergraph_ml(a_hat, p: int, seed: int = 0, epsilon: float = 0.01,
         return Partition.from_assignment(np.zeros(a_hat.n_rows, dtype=np.int64), weights, 1, epsilon)
     lab = community_labels(model, sweeps=sweeps) if labels is None else np.asarray(labels)
     _, lab = np.unique(lab, return_inverse=True)
-    coarse = coarse_column_nets(model, lab)
     cfg = PartitionConfig(p=p, epsilon=epsilon, seed=seed, fm_passes=fm_passes, restarts=restarts)
-    cpi = partition_hypergraph_fm(coarse, cfg)
+    if int(lab.max()) + 1 < 8 * p:
+        # too few communities to balance p parts (e.g. an expander): flat FM
+        h = graph_net_list(model) if kind == "gp" else column_net_model(model)
+        return (partition_graph_fm if kind == "gp" else partition_hypergraph_fm)(h, cfg)
+    if kind == "gp":
+        cpi = partition_graph_fm(coarse_graph_nets(model, lab), cfg)
+    else:
+        cpi = partition_hypergraph_fm(coarse_column_nets(model, lab), cfg)
     owner = cpi.assignment[lab]
     pi = Partition.from_assignment(owner, weights, p, epsilon)
     if not pi.is_balanced():
@@ -320,3 +353,18 @@ def partition_hypergraph(a_hat, p: int, seed: int = 0, epsilon: float = 0.01, di
     model = symmetrized(a_hat) if directed else a_hat
     cfg = PartitionConfig(p=p, epsilon=epsilon, seed=seed, fm_passes=fm_passes, restarts=restarts)
     return partition_hypergraph_fm(column_net_model(model), cfg)
+
+
+def partition_graph(a_hat, p: int, seed: int = 0, epsilon: float = 0.01, directed: bool | None = None,
+                    fm_passes: int = 8, restarts: int = 3) -> Partition:
+    """GP of a normalised adjacency: graph model of Â (of its symmetrised
+    pattern for directed inputs), as cli.py:184-185,226 builds it."""
+    if directed is None:
+        from .sparse import transpose_sparse
+
+        t = transpose_sparse(a_hat)
+        directed = not (np.array_equal(np.asarray(a_hat.row_offsets), t.row_offsets)
+                        and np.array_equal(np.asarray(a_hat.col_indices), t.col_indices))
+    model = symmetrized(a_hat) if directed else a_hat
+    cfg = PartitionConfig(p=p, epsilon=epsilon, seed=seed, fm_passes=fm_passes, restarts=restarts)
+    return partition_graph_fm(graph_net_list(model), cfg)
