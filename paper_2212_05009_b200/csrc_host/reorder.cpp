@@ -45,3 +45,45 @@ extern "C" int gcnb_label_propagation(int64_t n, const int64_t* rp, const int64_
   }
   return 0;
 }
+
+// Chain order of the communities: a maximum-adjacency (Prim-like) ordering of
+// the contracted community graph.  Starting from `start`, repeatedly place the
+// unplaced community with the largest total edge weight to the already-placed
+// set (ties: lowest id; disconnected remainder: lowest unplaced id).  Laying
+// communities out in this order puts the communities a row's off-community
+// neighbours live in next to it, so those gathers also stay in L2's reuse
+// window.  rank_out[c] = position of community c in the chain.
+#include <queue>
+#include <utility>
+
+extern "C" int gcnb_chain_order(int64_t C, const int64_t* ptr, const int64_t* adj, const double* w, int64_t start,
+                                int64_t* rank_out) {
+  if (C < 0 || !ptr || !rank_out || (C > 0 && (start < 0 || start >= C))) return 1;
+  std::vector<double> conn(C, 0.0);
+  std::vector<char> placed(C, 0);
+  using Item = std::pair<double, int64_t>;  // (weight, -id): max weight, then lowest id
+  std::priority_queue<Item> heap;
+  int64_t next = 0, scan = 0;
+  if (C > 0) heap.push({0.0, -start});
+  while (next < C) {
+    if (heap.empty()) {
+      while (placed[scan]) ++scan;
+      heap.push({0.0, -scan});
+    }
+    const Item it = heap.top();
+    heap.pop();
+    const int64_t v = -it.second;
+    if (placed[v] || it.first != conn[v]) continue;  // stale entry
+    placed[v] = 1;
+    rank_out[v] = next++;
+    for (int64_t e = ptr[v]; e < ptr[v + 1]; ++e) {
+      const int64_t u = adj[e];
+      if (u < 0 || u >= C) return 1;
+      if (!placed[u]) {
+        conn[u] += w[e];
+        heap.push({conn[u], -u});
+      }
+    }
+  }
+  return 0;
+}

@@ -407,7 +407,11 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
             pi = partition_graph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, labels=labels)
         else:
             pi = random_partition(wl["a_hat"].row_nnz(), PartitionConfig(p=world, seed=args.seed, epsilon=0.01))
-        box[0] = (pi.assignment, labels if args.locality == "on" else None)
+        if args.locality == "on":
+            from .locality import chain_keys
+
+            keys = chain_keys(wl["a_hat"], labels)
+        box[0] = (pi.assignment, keys if args.locality == "on" else None)
     dist.broadcast_object_list(box, src=0)
     owner = np.asarray(box[0][0], dtype=np.int64)
     row_labels = box[0][1]

@@ -57,6 +57,8 @@ def _load():
         lib.gcnb_hp_bisect.argtypes = [i32, i32, vp, vp, vp, vp, f64, i64, vp, i32, i32, i32, vp, vp]
         lib.gcnb_hp_bisect.restype = ctypes.c_int
         lib.gcnb_label_propagation.argtypes = [i64, vp, vp, i32, vp]
+        lib.gcnb_chain_order.argtypes = [i64, vp, vp, vp, i64, vp]
+        lib.gcnb_chain_order.restype = ctypes.c_int
         lib.gcnb_label_propagation.restype = ctypes.c_int
         _hlib = lib
     return _hlib

@@ -1,8 +1,10 @@
 """Locality ordering of each rank's rows (a layout choice).
 
 `community_labels` runs deterministic label propagation (csrc_host/reorder.cpp)
-on the symmetrised pattern; `rank_row_order` lays a rank's own rows out
-community by community (ties by global id).  Plans, halo order (sender, then
+on the symmetrised pattern; `chain_keys` orders the communities along a
+maximum-adjacency chain of the contracted community graph (so a row's
+off-community neighbours sit in nearby communities); `rank_row_order` lays a
+rank's own rows out by that key (ties by global id).  Plans, halo order (sender, then
 global id — what peers pack), results and the public `global_rows` mapping are
 unchanged; only the position of each own row in the rank's device blocks moves,
 so consecutive tiles gather neighbours that sit together in the feature block.
@@ -33,6 +35,36 @@ def community_labels(a, sweeps: int = 5) -> np.ndarray:
     if rc != 0:
         raise ValueError("label propagation: invalid input")
     return labels
+
+
+def chain_keys(a, labels: np.ndarray) -> np.ndarray:
+    """Per-vertex layout key: the chain position of the vertex's community
+    (gcnb_chain_order over the community graph, edge weight = number of Â
+    nonzeros between two communities, starting from the largest community)."""
+    _, lab = np.unique(np.asarray(labels), return_inverse=True)
+    C = int(lab.max()) + 1 if len(lab) else 0
+    ro = np.asarray(a.row_offsets, dtype=np.int64)
+    ci = np.asarray(a.col_indices, dtype=np.int64)
+    cu = np.repeat(lab, np.diff(ro))
+    cv = lab[ci]
+    off = cu != cv
+    key, cnt = np.unique(np.concatenate([cu[off] * C + cv[off], cv[off] * C + cu[off]]), return_counts=True)
+    src, dst = key // C, key % C
+    ptr = np.zeros(C + 1, dtype=np.int64)
+    np.cumsum(np.bincount(src, minlength=C), out=ptr[1:])
+    adj = np.ascontiguousarray(dst, dtype=np.int64)
+    w = np.ascontiguousarray(cnt, dtype=np.float64)
+    rank = np.empty(C, dtype=np.int64)
+    start = int(np.argmax(np.bincount(lab, minlength=C))) if C else 0
+    rc = hp._load().gcnb_chain_order(C, ptr.ctypes.data, adj.ctypes.data, w.ctypes.data, start, rank.ctypes.data)
+    if rc != 0:
+        raise ValueError("chain order: invalid community graph")
+    return rank[lab]
+
+
+def locality_keys(a, sweeps: int = 5) -> np.ndarray:
+    """community_labels + chain_keys: the row_labels the layout sorts by."""
+    return chain_keys(a, community_labels(a, sweeps=sweeps))
 
 
 def rank_row_order(rows: np.ndarray, labels: np.ndarray) -> np.ndarray:

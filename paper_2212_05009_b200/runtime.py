@@ -542,9 +542,9 @@ def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, 
         a_bwd, plan_bwd = a_hat, plan_fwd
     labels = None
     if locality:
-        from .locality import community_labels
+        from .locality import locality_keys
 
-        labels = community_labels(a_hat)
+        labels = locality_keys(a_hat)
     states = []
     for m in range(plan_fwd.p):
         lay = build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, m, row_labels=labels)

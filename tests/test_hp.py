@@ -109,3 +109,34 @@ def test_label_propagation_recovers_blocks():
     assert len(blocks[0]) == 1 and len(blocks[1]) == 1 and blocks[0] != blocks[1]
     order = rank_row_order(np.arange(n), lab)
     assert sorted(order.tolist()) == list(range(n))
+
+
+def test_chain_keys_place_adjacent_communities_next_to_each_other():
+    from paper_2212_05009_b200.locality import chain_keys
+
+    # 12 cliques of 6 vertices on a ring (clique c linked to c±1 by 3 edges),
+    # community ids scrambled: every chain entry must touch the placed set
+    k, s = 12, 6
+    rows, cols = [], []
+    for c in range(k):
+        for i in range(s):
+            for j in range(s):
+                if i != j:
+                    rows.append(c * s + i)
+                    cols.append(c * s + j)
+        nxt = (c + 1) % k
+        for t in range(3):
+            rows += [c * s + t, nxt * s + t]
+            cols += [nxt * s + t, c * s + t]
+    n = k * s
+    a = gb.normalize_adjacency(gb.CsrMatrix.from_coo(n, n, rows, cols, np.ones(len(rows))))
+    scramble = np.random.default_rng(1).permutation(k)
+    labels = scramble[np.arange(n) // s]
+    keys = chain_keys(a, labels)
+    ring_pos = keys[np.arange(k) * s]            # chain position of clique c
+    assert sorted(ring_pos.tolist()) == list(range(k))
+    assert np.all(keys == ring_pos[np.arange(n) // s])
+    order = np.argsort(ring_pos)                 # cliques in chain order
+    for t in range(1, k):                        # each is adjacent to an already-placed clique
+        placed = set(order[:t].tolist())
+        assert (order[t] + 1) % k in placed or (order[t] - 1) % k in placed
