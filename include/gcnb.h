@@ -128,6 +128,12 @@ int gcnb_dense_f32(const float* x, int32_t ldx, const int32_t* rows, int32_t n_r
                    int32_t d_in, const float* w, int32_t d_out, float* y, int32_t ldy,
                    int32_t act, void* stream);
 
+/* Dense-transform engine selection (process-wide): 0 = auto (tcgen05 3xTF32
+ * for d_in, d_out >= 32, register-blocked SIMT fp32 otherwise), 1 = SIMT fp32
+ * everywhere, 2 = tcgen05 wherever the tile fits shared memory.  Both engines
+ * meet the 1e-4 fp32 bar; they differ in the last bits. */
+int gcnb_set_dense_mode(int32_t mode);
+
 /* runtime._bwd_compute (runtime.py:344-356) for the row list `rows`:
  *   agg[r]   = A_back[r,:]·G                       (G extended, d_k wide)
  *   G_prev[r] = (agg[r]·W^T) ⊙ act'(H_prev[r])     if g_prev != NULL (k > 1)

@@ -27,6 +27,17 @@ int num_sms();
 bool dense_blocked_applies(int d_in, int d_out);
 int launch_dense_blocked(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
                          float* y, int ldy, int act, cudaStream_t st);
+// dense_tc.cu: tcgen05 3xTF32 transform for the wide dense layers
+bool dense_tc_applies(int d_in, int d_out);
+// w_nk != nullptr: B = w_nk stored N×K (row stride ld_wnk) instead of w (K×N);
+// hmask != nullptr: epilogue y = acc ⊙ σ'(hmask) (backward) instead of act(acc)
+int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
+                    float* y, int ldy, int act, cudaStream_t st, const float* w_nk = nullptr, int ld_wnk = 0,
+                    const float* hmask = nullptr, int ldhm = 0);
+bool dw_tc_applies(int d_prev, int d_k);
+int dw_tc_grid(int n_rows);
+int launch_dw_tc(const float* h, int ldh, int d_prev, const float* a, int lda, int d_k, const int* rows, int n_rows,
+                 float* partials, int n_slots, cudaStream_t st);
 
 // After every <<<>>> launch: surface launch errors, count the launch.
 #define GCNB_AFTER_LAUNCH(what)                                         \

@@ -764,6 +764,8 @@ extern "C" int gcnb_dense_f32(const float* x, int32_t ldx, const int32_t* rows, 
                "dense: row strides must be multiples of 4 and cover the widths");
   GCNB_REQUIRE(x && w && y && aligned16(x) && aligned16(w) && aligned16(y), "dense: operands must be 16-byte aligned");
   if (n_rows == 0) return GCNB_OK;
+  if (dense_tc_applies(d_in, d_out))
+    return launch_dense_tc(x, ldx, rows, n_rows, d_in, w, d_out, y, ldy, act, (cudaStream_t)stream);
   if (dense_blocked_applies(d_in, d_out))
     return launch_dense_blocked(x, ldx, rows, n_rows, d_in, w, d_out, y, ldy, act, (cudaStream_t)stream);
   return launch_fwd_gemm(false, nullptr, nullptr, nullptr, rows, n_rows, x, ldx, d_in, w, d_out, y, ldy, act,
@@ -803,6 +805,15 @@ extern "C" int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
     if (int rc = launch_agg(row_ptr, col, val, rows, n_rows, g, ldg, d_k, workspace, round4(d_k), -1, st,
                             "bwd layer (aggregate)"))
       return rc;
+    if (dw_tc_applies(d_prev, d_k) && (!g_prev || dense_tc_applies(d_k, d_prev))) {
+      // tensor-core epilogue: G_prev = (agg·Wᵀ) ⊙ σ'(H_prev) and the ΔW partials, 3xTF32
+      if (g_prev) {
+        if (int rc = launch_dense_tc(workspace, round4(d_k), rows, n_rows, d_k, nullptr, d_prev, g_prev, ldgp, act, st,
+                                     w, round4(d_k), h_prev, ldhp))
+          return rc;
+      }
+      return launch_dw_tc(h_prev, ldhp, d_prev, workspace, round4(d_k), d_k, rows, n_rows, dw_partials, plan.grid, st);
+    }
     plan.fn<<<plan.grid, NT, plan.smem, st>>>(nullptr, nullptr, nullptr, rows, n_rows, workspace, round4(d_k), d_k,
                                               h_prev, ldhp, d_prev, w, g_prev, ldgp, act, dw_partials, plan.T);
     GCNB_AFTER_LAUNCH("bwd layer (dense epilogue)");

@@ -132,8 +132,16 @@ def test_fwd_layer_aggregate_only_relu_and_rows():
     close(got[rows], want[rows])
 
 
-@pytest.mark.parametrize("d_in,d_out", [(16, 8), (100, 128), (128, 47), (3, 5)])
-def test_dense_transform(d_in, d_out):
+@pytest.fixture
+def dense_mode(request):
+    _lib.call("gcnb_set_dense_mode", request.param)
+    yield request.param
+    _lib.call("gcnb_set_dense_mode", 0)
+
+
+@pytest.mark.parametrize("dense_mode", [0, 1, 2], indirect=True, ids=["auto", "simt", "tcgen05"])
+@pytest.mark.parametrize("d_in,d_out", [(16, 8), (100, 128), (128, 47), (3, 5), (64, 256), (33, 40)])
+def test_dense_transform(d_in, d_out, dense_mode):
     x = np.random.default_rng(9).standard_normal((3001, d_in))
     w = np.random.default_rng(10).standard_normal((d_in, d_out))
     d = dev()
@@ -150,6 +158,30 @@ def test_dense_transform(d_in, d_out):
     got = devmem.download(yd2, 3001, d_out)
     close(got[rows], np.maximum(o.dmm(x, w)[rows], 0))
     assert np.all(got[np.setdiff1d(np.arange(3001), rows)] == 0)
+
+
+@pytest.mark.parametrize("d_in,d_out", [(100, 128), (128, 47)])
+def test_dense_tcgen05_many_tiles_matches_simt(d_in, d_out):
+    """Persistent tcgen05 kernel over many 128-row tiles per CTA (double-buffered
+    stages, ragged last tile): 3xTF32 and the exact-fp32 SIMT engine both agree
+    with the fp64 oracle within TOL, and tcgen05 reruns are bit-identical."""
+    n = 128 * 148 * 3 + 77
+    x = np.random.default_rng(11).standard_normal((n, d_in))
+    w = np.random.default_rng(12).uniform(-0.2, 0.2, (d_in, d_out))
+    d = dev()
+    xd, wd = devmem.upload_dense(x, d), devmem.upload_dense(w, d)
+    outs = []
+    for mode in (2, 2, 1):
+        _lib.call("gcnb_set_dense_mode", mode)
+        yd = devmem.empty_rows(n, d_out, d)
+        _lib.call("gcnb_dense_f32", xd.data_ptr(), xd.shape[1], None, n, d_in, wd.data_ptr(), d_out, yd.data_ptr(),
+                  yd.shape[1], _lib.ACT["relu"], devmem.stream_handle(None, d))
+        outs.append(devmem.download(yd, n, d_out))
+    _lib.call("gcnb_set_dense_mode", 0)
+    want = np.maximum(o.dmm(x, w), 0)
+    close(outs[0], want)
+    close(outs[2], want)
+    assert np.array_equal(outs[0], outs[1])
 
 
 def _bwd(a, g, hp, w, act, with_gp, rows=None, split=True):
@@ -193,9 +225,12 @@ def test_bwd_layer(d_p, d_k, act):
     close(dw_only, o.dmm_tn(hp, agg))
 
 
+@pytest.mark.parametrize("dense_mode", [1], indirect=True, ids=["simt"])
 @pytest.mark.parametrize("d_p,d_k", [(100, 128), (128, 47)])
-def test_bwd_split_equals_fused_bitwise(d_p, d_k):
-    """The two-kernel (workspace) form computes exactly the fused kernel's values."""
+def test_bwd_split_equals_fused_bitwise(d_p, d_k, dense_mode):
+    """With the SIMT engine, the two-kernel (workspace) form computes exactly the
+    fused kernel's values (the tcgen05 epilogue is checked against the oracle in
+    test_bwd_layer and test_bwd_tcgen05_many_tiles)."""
     assert _lib.bwd_workspace_ld(d_p, d_k) > 0
     a = rand_csr(2000, 2000, 0.005, 5)
     rng = np.random.default_rng(1)
@@ -204,6 +239,32 @@ def test_bwd_split_equals_fused_bitwise(d_p, d_k):
     s = _bwd(a, g, hp, w, "relu", True, rows, split=True)
     f = _bwd(a, g, hp, w, "relu", True, rows, split=False)
     assert np.array_equal(s[0], f[0]) and np.array_equal(s[1], f[1])
+
+
+@pytest.mark.parametrize("d_p,d_k", [(100, 128), (128, 47)])
+def test_bwd_tcgen05_many_tiles(d_p, d_k):
+    """Split backward on the tcgen05 epilogue over many 64-row ΔW tiles per CTA and
+    a ragged tail: G_prev and ΔW within TOL of the oracle, ΔW deterministic,
+    and SIMT and tcgen05 engines agree within TOL."""
+    n = 64 * 148 * 3 + 29
+    rng = np.random.default_rng(21)
+    a = rand_csr(n, n, 6.0 / n, 22)
+    g = rng.standard_normal((n, d_k))
+    hp = np.maximum(rng.standard_normal((n, d_p)), 0)
+    w = rng.uniform(-0.2, 0.2, (d_p, d_k))
+    gp, dw, _ = _bwd(a, g, hp, w, "relu", True)
+    gp2, dw2, _ = _bwd(a, g, hp, w, "relu", True)
+    assert np.array_equal(dw, dw2) and np.array_equal(gp, gp2)
+    agg = o.spmm(a, g)
+    close(gp, o.dmm(agg, w.T.copy()) * (hp > 0))
+    close(dw, o.dmm_tn(hp, agg))
+    _lib.call("gcnb_set_dense_mode", 1)
+    try:
+        gps, dws, _ = _bwd(a, g, hp, w, "relu", True)
+    finally:
+        _lib.call("gcnb_set_dense_mode", 0)
+    close(dw, dws)
+    close(gp, gps)
 
 
 def test_bwd_layer_row_subsets_sum_to_full():
