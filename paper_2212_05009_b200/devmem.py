@@ -32,7 +32,17 @@ def device(dev=None) -> torch.device:
 
 
 def ld_of(d: int) -> int:
+    """Row stride of the small packed blocks (W, ΔW, partials): round4(d)."""
     return (int(d) + 3) // 4 * 4
+
+
+def feat_ld(d: int) -> int:
+    """Row stride of the gathered feature blocks: a multiple of 8 floats for
+    d > 4, so every row starts on a 32-byte sector and a row gather touches
+    exactly ceil(4d/32) sectors (a 400-byte row at a 16-byte offset costs 16
+    sectors in quarter-warp requests instead of 13)."""
+    d = int(d)
+    return 4 if d <= 4 else (d + 7) // 8 * 8
 
 
 def stream_handle(stream, dev) -> int:

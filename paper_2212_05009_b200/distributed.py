@@ -36,6 +36,8 @@ import time
 
 import numpy as np
 
+from . import devmem
+
 from . import _lib
 from .comm import build_comm_plan
 from .layout import build_rank_layout
@@ -72,8 +74,8 @@ def arena_layout(n_own: int, r_fwd: int, r_bwd: int, dims, transform_first, p: i
         cur += (int(nbytes) + ALIGN - 1) // ALIGN * ALIGN
 
     for k in range(1, L + 1):
-        take(f"xext{k}", (n_own + r_fwd) * ld_of(fw[k]) * 4)
-        take(f"gext{k}", (n_own + r_bwd) * ld_of(bw[k]) * 4)
+        take(f"xext{k}", (n_own + r_fwd) * devmem.feat_ld(fw[k]) * 4)
+        take(f"gext{k}", (n_own + r_bwd) * devmem.feat_ld(bw[k]) * 4)
     slot = n_pack + 4
     take("slots", 2 * p * slot * 4)
     take("flags_halo", 8 * p)
@@ -187,7 +189,7 @@ class Arena:
     def rows_alloc(self, name: str, rows: int, width: int):
         import torch
 
-        return self.tensor(name, (rows, ld_of(width)), torch.float32)
+        return self.tensor(name, (rows, devmem.feat_ld(width)), torch.float32)
 
     def handle(self) -> bytes:
         buf = ctypes.create_string_buffer(64)

@@ -213,7 +213,7 @@ class ProcState:
         (default: private device memory; distributed.py passes an IPC arena)."""
         if alloc is None:
             def alloc(name, rows, width):
-                return devmem.empty_rows(rows, width, dev)
+                return devmem.empty_rows(rows, width, dev, ld=devmem.feat_ld(width))
         self.rank = layout.rank
         self.global_rows = layout.global_rows
         self.plan_fwd = plan_fwd
