@@ -56,12 +56,15 @@ __global__ void __launch_bounds__(NT) k_pack(const float4* __restrict__ X4, int 
     reinterpret_cast<float4*>(a.dst[s])[(size_t)(e - a.seg_ptr[s]) * ldd4 + ch] = v;
   }
   if (!signal) return;
-  // Make this thread's (possibly remote) stores visible system-wide, then
-  // elect the last block to ring the doorbells.
-  __threadfence_system();
+  // The block's (possibly remote) stores happen-before thread 0's system-scope
+  // fence through the barrier (fences are cumulative), so one fence per block
+  // suffices; the last block to arrive rings the doorbells.
   __syncthreads();
   __shared__ int last;
-  if (threadIdx.x == 0) last = (atomicAdd(counter, 1) == (int)gridDim.x - 1);
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    last = (atomicAdd(counter, 1) == (int)gridDim.x - 1);
+  }
   __syncthreads();
   if (last && threadIdx.x == 0) {
     __threadfence_system();
@@ -211,10 +214,12 @@ __global__ void __launch_bounds__(NT) k_push(const float4* __restrict__ src, lon
     const long long j = t - (long long)d * n4;
     a.dst[d][j] = __ldg(src + j);
   }
-  __threadfence_system();
-  __syncthreads();
+  __syncthreads();  // see k_pack: one cumulative system fence per block
   __shared__ int last;
-  if (threadIdx.x == 0) last = (atomicAdd(counter, 1) == (int)gridDim.x - 1);
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    last = (atomicAdd(counter, 1) == (int)gridDim.x - 1);
+  }
   __syncthreads();
   if (last && threadIdx.x == 0) {
     __threadfence_system();
@@ -310,7 +315,8 @@ extern "C" int gcnb_pack_rows_f32(const float* x, int32_t ldx, int32_t d, const 
   GCNB_REQUIRE(total == 0 || (idx && aligned16(x)), "pack: index list and 16-byte aligned source required");
   const int c4 = round4(d) / 4;
   const long long work = (long long)total * c4;
-  const int grid = (int)std::max<long long>(1, std::min<long long>((work + NT - 1) / NT, num_sms() * 8));
+  // a few rows per thread: fewer blocks → fewer fences and counter arrivals
+  const int grid = (int)std::max<long long>(1, std::min<long long>((work + 4 * NT - 1) / (4 * NT), num_sms() * 2));
   k_pack<<<grid, NT, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4*>(x), ldx / 4, c4, idx, a, ld_dst / 4,
                                                 counter, signal);
   GCNB_AFTER_LAUNCH("pack rows");

@@ -16,25 +16,31 @@ extern "C" int gcnb_label_propagation(int64_t n, const int64_t* rp, const int64_
                                       int64_t* labels) {
   if (n < 0 || !rp || !ci || !labels || sweeps < 0) return 1;
   for (int64_t v = 0; v < n; ++v) labels[v] = v;
-  std::vector<int64_t> nb;
+  // O(deg) label histogram per vertex: counts in a dense array, reset through
+  // the list of labels touched (the winner is the most frequent label, ties
+  // to the smallest — the same choice as an ascending scan of the sorted list)
+  std::vector<int32_t> cnt(n, 0);
+  std::vector<int64_t> touched;
   for (int s = 0; s < sweeps; ++s) {
     int64_t changed = 0;
     for (int64_t v = 0; v < n; ++v) {
-      nb.clear();
-      nb.push_back(labels[v]);
-      for (int64_t e = rp[v]; e < rp[v + 1]; ++e)
-        if (ci[e] != v) nb.push_back(labels[ci[e]]);
-      std::sort(nb.begin(), nb.end());
-      int64_t best = labels[v], best_cnt = 0;
-      for (size_t i = 0; i < nb.size();) {
-        size_t j = i;
-        while (j < nb.size() && nb[j] == nb[i]) ++j;
-        const int64_t cnt = (int64_t)(j - i);
-        if (cnt > best_cnt) {  // ascending scan: ties keep the smaller label
-          best_cnt = cnt;
-          best = nb[i];
+      touched.clear();
+      touched.push_back(labels[v]);
+      cnt[labels[v]] = 1;
+      for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+        const int64_t u = ci[e];
+        if (u == v) continue;
+        const int64_t l = labels[u];
+        if (cnt[l]++ == 0) touched.push_back(l);
+      }
+      int64_t best = labels[v];
+      int32_t best_cnt = 0;
+      for (const int64_t l : touched) {
+        if (cnt[l] > best_cnt || (cnt[l] == best_cnt && l < best)) {
+          best_cnt = cnt[l];
+          best = l;
         }
-        i = j;
+        cnt[l] = 0;
       }
       if (best != labels[v]) {
         labels[v] = best;

@@ -205,10 +205,17 @@ class Arena:
 class DistributedTrainer:
     """Full-batch training of this process's rank; collective over torch.distributed."""
 
+    # per-exchange halo below which overlapping (interior launch, wait, boundary
+    # launch) costs more in launch latency than the transfer it would hide
+    OVERLAP_MIN_BYTES = 4 << 20
+
     def __init__(self, a_hat, h0, owner, p: int, model, labels, directed: bool, device, timeout_ms: int = 20000,
-                 row_labels=None):
+                 row_labels=None, overlap: bool | None = None):
         """row_labels: optional per-vertex community labels for the locality
-        layout of own rows (locality.py); None keeps ascending global ids."""
+        layout of own rows (locality.py); None keeps ascending global ids.
+        overlap: split each layer into interior rows (computed while the halo
+        is in flight) and boundary rows; None = only when this rank's largest
+        incoming halo exceeds OVERLAP_MIN_BYTES."""
         import torch
         import torch.distributed as dist
 
@@ -224,6 +231,12 @@ class DistributedTrainer:
         dims = tuple(int(d) for d in model.dims)
         L = len(dims) - 1
         tf = [False] + [dims[k] < dims[k - 1] for k in range(1, L + 1)]
+        if overlap is None:
+            fw, bw = widths(dims, tf)
+            biggest = max(max(layout.fwd.n_halo * devmem.ld_of(fw[k]), layout.bwd.n_halo * devmem.ld_of(bw[k]))
+                          for k in range(1, L + 1)) * 4
+            overlap = biggest > self.OVERLAP_MIN_BYTES
+        self.overlap = bool(overlap)
         sizes = [dims[k - 1] * ld_of(dims[k]) for k in range(1, L + 1)]
         n_pack = int(sum(sizes))
         n_own = len(layout.global_rows)
@@ -277,11 +290,14 @@ class DistributedTrainer:
         self.graphs = {}
 
     # -- one epoch ------------------------------------------------------------
-    def _wait(self, flags, expected, srcs):
+    def _wait(self, flags, expected, srcs, name: str = "wait"):
         if not srcs:
             return
-        _lib.call("gcnb_wait_flags", flags.data_ptr(), _lib.int_array(srcs), len(srcs), expected.data_ptr(),
-                  self.err.data_ptr(), self.timeout_ms, self.st.stream())
+        from .profiling import span
+
+        with span(name, 0, 0, self.st.stream()):
+            _lib.call("gcnb_wait_flags", flags.data_ptr(), _lib.int_array(srcs), len(srcs), expected.data_ptr(),
+                      self.err.data_ptr(), self.timeout_ms, self.st.stream())
 
     def enqueue_epoch(self, parity: int, comm: bool = True) -> None:
         st, L = self.st, self.st.n_layers
@@ -290,19 +306,25 @@ class DistributedTrainer:
             st.fwd_transform(k)
             if comm:
                 st.pack_to("fwd", k, self.fwd_bases[k], flags=self.halo_flag_fwd, counter=cnt)
-            st.fwd_compute(k, "interior")
+            if self.overlap:
+                st.fwd_compute(k, "interior")
             if comm:
-                self._wait(self.flags_halo, self.expected_halo, self.sched.fwd_src)
-            st.fwd_compute(k, "boundary")
+                self._wait(self.flags_halo, self.expected_halo, self.sched.fwd_src, f"wait_fwd{k}")
+            st.fwd_compute(k, "boundary" if self.overlap else "all")
         st.loss_grad(1.0 / self.n_lab)
         for k in range(L, 0, -1):
             if comm:
                 st.pack_to("bwd", k, self.bwd_bases[k], flags=self.halo_flag_bwd, counter=cnt)
-            gi = st.bwd_compute(k, "interior", slot=0)
-            if comm:
-                self._wait(self.flags_halo, self.expected_halo, self.sched.bwd_src)
-            gb = st.bwd_compute(k, "boundary", slot=gi)
-            st.reduce_dw(k, gi + gb)
+            if self.overlap:
+                gi = st.bwd_compute(k, "interior", slot=0)
+                if comm:
+                    self._wait(self.flags_halo, self.expected_halo, self.sched.bwd_src, f"wait_bwd{k}")
+                gb = st.bwd_compute(k, "boundary", slot=gi)
+                st.reduce_dw(k, gi + gb)
+            else:
+                if comm:
+                    self._wait(self.flags_halo, self.expected_halo, self.sched.bwd_src, f"wait_bwd{k}")
+                st.reduce_dw(k, st.bwd_compute(k, "all", slot=0))
         n_tot = st.n_pack + 4
         from .profiling import span
 
@@ -310,7 +332,7 @@ class DistributedTrainer:
             with span("allreduce_push", 4 * n_tot * self.p, 0, st.stream()):
                 _lib.call("gcnb_push_f32", st.dwpack.data_ptr(), n_tot, _lib.ptr_array(self.ar_dst[parity]),
                           _lib.ptr_array(self.ar_flag), self.p, cnt, st.stream())
-            self._wait(self.flags_ar, self.expected_ar, self.ar_srcs)
+            self._wait(self.flags_ar, self.expected_ar, self.ar_srcs, "wait_allreduce")
             slots = self.slots[parity]
             _lib.call("gcnb_sum_slots_f32", slots.data_ptr(), self.p, self.slot, st.n_pack, st.dwsum_pack.data_ptr(),
                       self.loss_total.data_ptr(), st.stream())
@@ -388,25 +410,28 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
         if args.locality == "on" or args.partition.endswith("-ml"):
             from .locality import community_labels
 
-            labels = community_labels(wl["a_hat"])
+            labels = community_labels(wl["a_hat"], symmetric=None if wl["directed"] else True)
         if args.partition == "hp":
             from .hp import partition_hypergraph
 
             # reference defaults are 8 FM passes x 3 BFS restarts; 4 x 1 keeps
             # a 0.4 M-vertex bisection tree within ~1-2 minutes
-            pi = partition_hypergraph(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1)
+            pi = partition_hypergraph(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1,
+                                      directed=wl["directed"])
         elif args.partition == "hp-ml":
             from .hp import partition_hypergraph_ml
 
-            pi = partition_hypergraph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, labels=labels)
+            pi = partition_hypergraph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, labels=labels,
+                                         directed=wl["directed"])
         elif args.partition == "gp":
             from .hp import partition_graph
 
-            pi = partition_graph(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1)
+            pi = partition_graph(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, directed=wl["directed"])
         elif args.partition == "gp-ml":
             from .hp import partition_graph_ml
 
-            pi = partition_graph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, labels=labels)
+            pi = partition_graph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, labels=labels,
+                                    directed=wl["directed"])
         else:
             pi = random_partition(wl["a_hat"].row_nnz(), PartitionConfig(p=world, seed=args.seed, epsilon=0.01))
         if args.locality == "on":
@@ -418,8 +443,9 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
     owner = np.asarray(box[0][0], dtype=np.int64)
     row_labels = box[0][1]
     t_part = time.perf_counter() - t0
+    ov = {"auto": None, "on": True, "off": False}[getattr(args, "overlap", "auto")]
     tr = DistributedTrainer(wl["a_hat"], wl["h0"], owner, world, wl["model"], wl["labels"], wl["directed"],
-                            device, row_labels=row_labels)
+                            device, row_labels=row_labels, overlap=ov)
     st = tr.st
     from . import _lib as L_
 
@@ -434,9 +460,13 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
     tr.check()
     # the next timed epoch index must continue the parity sequence
     start_parity = max(args.warmup, 3) % 2
+    # timed graphs carry no event nodes; the instrumented twins (per-kernel spans)
+    # are replayed separately for the kernel table
     timers = {0: profiling.KernelTimer(), 1: profiling.KernelTimer()}
-    tr.capture(0, 0, True, timers[0])
-    tr.capture(1, 1, True, timers[1])
+    tr.capture(0, 0, True, None)
+    tr.capture(1, 1, True, None)
+    tr.capture("i0", 0, True, timers[0])
+    tr.capture("i1", 1, True, timers[1])
     tr.capture("compute", 0, False, None)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -452,11 +482,21 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
             tr.graphs[q].replay()
             evs[i][1].record()
             evs[i][1].synchronize()
-            rows.extend(timers[q].results())
     torch.cuda.synchronize()
     dist.barrier()
     tr.check()
     ms_rank = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    # instrumented replays (same epochs, event nodes around every kernel) for the kernel table;
+    # the parity sequence continues so every slot/doorbell count stays consistent
+    n_inst = min(args.steps, 10)
+    for i in range(n_inst):
+        q = (start_parity + args.steps + i) % 2
+        flush.zero_()
+        tr.device_barrier()
+        tr.graphs[f"i{q}"].replay()
+        torch.cuda.synchronize()
+        rows.extend(timers[q].results())
+    tr.check()
     # compute-only epochs (no sends, waits or allreduce) for the exposed-communication share
     cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for i in range(args.steps):
@@ -471,7 +511,7 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
     d0 = wl["dims"][0]
     h0_pinned = torch.from_numpy(np.asarray(wl["h0"][tr.layout.global_rows], dtype=np.float32)).pin_memory()
     e2e = []
-    par = (start_parity + args.steps) % 2
+    par = (start_parity + args.steps + n_inst) % 2
     dist.barrier()
     for i in range(0 if args.kernels_only else max(3, min(args.steps, 20))):
         torch.cuda.synchronize()
@@ -489,8 +529,15 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
                          reference_words_per_epoch(tr.layout, st.dims)], dtype=torch.float64)
     dist.all_reduce(halo, op=dist.ReduceOp.SUM)
     peak, peak_kind = measured_peaks()
-    compute_rows = [r for r in rows if not r[0].startswith(("pack", "allreduce"))]
-    kname, achieved, kms, kbytes, table = roofline_summary(compute_rows, peak, peak_kind, args.steps)
+    compute_rows = [r for r in rows if not r[0].startswith(("pack", "allreduce", "wait"))]
+    exch = {}
+    for r in rows:
+        if r[0].startswith(("pack", "allreduce", "wait")):
+            e = exch.setdefault(r[0], [0.0, 0])
+            e[0] += r[3]
+            e[1] += 1
+    exchange_ms = {k: round(v[0] / v[1], 5) for k, v in sorted(exch.items())}
+    kname, achieved, kms, kbytes, table = roofline_summary(compute_rows, peak, peak_kind, n_inst)
     pack = [r for r in rows if r[0].startswith("pack")]
     nvl = None
     if pack:
@@ -507,7 +554,8 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
                    "directed": wl["directed"], "partition": args.partition, "partition_s": round(t_part, 2),
                    "locality": args.locality,
                    "l2": "flushed (512 MiB write) before every step", "graph": True, "seed": args.seed,
-                   "transport": "NVLink peer stores + doorbells (CUDA IPC), P2P allreduce"},
+                   "transport": "NVLink peer stores + doorbells (CUDA IPC), P2P allreduce",
+                   "overlap": tr.overlap},
         "e2e": {"value": round(e2e_max, 4), "unit": UNIT,
                 "h2d_bytes_per_step": int(h0_pinned.numel() * 4), "d2h_bytes_per_step": 8},
         "gpu_launches": int(launches * args.steps),
@@ -518,6 +566,7 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
         "halo_bytes_per_epoch": int(halo[0].item()), "reference_words_per_epoch": int(halo[1].item()),
         "exposed_comm_pct": round(100.0 * max(0.0, ms - msc) / ms, 2), "compute_only_ms": round(msc, 4),
         "nvlink_pack_gbs_rank0": nvl,
+        "exchange_ms_rank0": exchange_ms,
         "cpu_baseline": None,
         "clocks": clk,
     }

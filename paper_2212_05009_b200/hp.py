@@ -60,6 +60,8 @@ def _load():
         lib.gcnb_chain_order.argtypes = [i64, vp, vp, vp, i64, vp]
         lib.gcnb_chain_order.restype = ctypes.c_int
         lib.gcnb_label_propagation.restype = ctypes.c_int
+        lib.gcnb_csr_transpose.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp]
+        lib.gcnb_csr_transpose.restype = ctypes.c_int
         _hlib = lib
     return _hlib
 

@@ -17,15 +17,17 @@ import numpy as np
 from . import hp
 
 
-def community_labels(a, sweeps: int = 5) -> np.ndarray:
+def community_labels(a, sweeps: int = 5, symmetric: bool | None = None) -> np.ndarray:
+    """symmetric: whether Â's pattern is symmetric (None: check)."""
     ro = np.ascontiguousarray(a.row_offsets, dtype=np.int64)
     ci = np.ascontiguousarray(a.col_indices, dtype=np.int64)
-    ro_t = a.row_offsets
-    # label propagation wants a symmetric pattern: use Â ∪ Âᵀ for directed inputs
-    from .sparse import transpose_sparse
+    if symmetric is None:
+        from .sparse import transpose_sparse
 
-    t = transpose_sparse(a)
-    if not (np.array_equal(ro_t, t.row_offsets) and np.array_equal(a.col_indices, t.col_indices)):
+        t = transpose_sparse(a)
+        symmetric = np.array_equal(a.row_offsets, t.row_offsets) and np.array_equal(a.col_indices, t.col_indices)
+    # label propagation wants a symmetric pattern: use Â ∪ Âᵀ for directed inputs
+    if not symmetric:
         s = hp.symmetrized(a)
         ro = np.ascontiguousarray(s.row_offsets, dtype=np.int64)
         ci = np.ascontiguousarray(s.col_indices, dtype=np.int64)
@@ -62,9 +64,9 @@ def chain_keys(a, labels: np.ndarray) -> np.ndarray:
     return rank[lab]
 
 
-def locality_keys(a, sweeps: int = 5) -> np.ndarray:
+def locality_keys(a, sweeps: int = 5, symmetric: bool | None = None) -> np.ndarray:
     """community_labels + chain_keys: the row_labels the layout sorts by."""
-    return chain_keys(a, community_labels(a, sweeps=sweeps))
+    return chain_keys(a, community_labels(a, sweeps=sweeps, symmetric=symmetric))
 
 
 def rank_row_order(rows: np.ndarray, labels: np.ndarray) -> np.ndarray:

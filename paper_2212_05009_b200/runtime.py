@@ -544,7 +544,7 @@ def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, 
     if locality:
         from .locality import locality_keys
 
-        labels = locality_keys(a_hat)
+        labels = locality_keys(a_hat, symmetric=None if directed else True)
     states = []
     for m in range(plan_fwd.p):
         lay = build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, m, row_labels=labels)

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--epochs", type=int, default=3)
     ap.add_argument("--n", type=int, default=4000)
     ap.add_argument("--graph", action="store_true", help="replay captured CUDA graphs")
+    ap.add_argument("--overlap", default="auto", choices=("auto", "on", "off"))
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank)))
@@ -41,7 +42,8 @@ def main():
     labels = gb.LabelSet(ids, y, dims[-1])
     model = gb.init_model(dims, 5)
     pi = gb.random_partition(a_hat.row_nnz(), gb.PartitionConfig(p=world, seed=5, epsilon=0.05))
-    tr = DistributedTrainer(a_hat, h0, pi.assignment, world, model, labels, args.directed, dev, timeout_ms=10000)
+    tr = DistributedTrainer(a_hat, h0, pi.assignment, world, model, labels, args.directed, dev, timeout_ms=10000,
+                            overlap={"auto": None, "on": True, "off": False}[args.overlap])
     losses = []
     if args.graph:
         tr.capture(0, 0)

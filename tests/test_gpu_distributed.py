@@ -15,13 +15,15 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-@pytest.mark.parametrize("extra", [[], ["--directed"], ["--directed", "--graph", "--epochs", "4"]])
+@pytest.mark.parametrize("extra", [["--overlap", "on"], ["--directed", "--overlap", "on"],
+                                   ["--directed", "--graph", "--epochs", "4", "--overlap", "on"],
+                                   ["--directed", "--graph", "--epochs", "4", "--overlap", "off"]])
 def test_torchrun_parity(extra):
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + len(extra)), str(ROOT / "scripts" / "dist_check.py"),
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + sum(map(ord, " ".join(extra))) % 300), str(ROOT / "scripts" / "dist_check.py"),
            *extra]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, "OMP_NUM_THREADS": "1"})
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
