@@ -2,12 +2,18 @@
 """Benchmark: full-batch GCN training epoch time (BASELINE.json metric
 "GCN ms/epoch at 1/2/4/8 B200; SpMM HBM GB/s; halo bytes & exposed comm %").
 
-Default workload (N=1): BASELINE config[1] — 2-layer GCN (dims 16,16,8) on the
-amazon0601-shaped directed synthetic graph (403,394 vertices, 3,387,388 arcs).
+Default workload: north_star's target line — full-batch 2-layer GCN (dims
+100,128,47) on the ogbn-products-shaped synthetic graph (2,449,029 vertices,
+61,859,140 undirected pairs, 126 M nnz(Â)) with HP partitioning (hp-ml) for
+N>1, the largest single-GPU configuration of BASELINE.json (config[3] shape;
+`--workload products3` is its 3-layer variant).  BASELINE config[1] is
+`--workload amazon0601` (403 K vertices, dims 16,16,8): a 0.25 ms epoch that
+is launch/latency-bound and does not strong-scale.
 A *step* is one epoch: forward over both layers, loss, backward, ΔW
 allreduce and SGD update, all on the device.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload amazon0601|config1|roadnet|products]
+    python bench.py [--gpus N] [--steps K] [--warmup W]
+                    [--workload products|products3|amazon0601|roadnet|config1]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   (one process per GPU)
     python bench.py --impl reference ...   (the reference algorithm on host cores: oracle port)
 
@@ -43,7 +49,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="amazon0601")
+    ap.add_argument("--workload", default="products", choices=("products", "products3", "amazon0601", "roadnet",
+                                                                 "config1"))
     ap.add_argument("--partition", default="hp-ml", choices=("rp", "hp", "hp-ml", "gp", "gp-ml"),
                     help="row partition for N>1 (BASELINE config[1] names HP): hp = the reference's flat "
                          "recursive-bisection FM (C++), hp-ml = the same FM on label-propagation clusters; "

@@ -25,3 +25,14 @@ extern "C" int gcnb_csr_transpose(int64_t n_rows, int64_t n_cols, const int64_t*
     }
   return 0;
 }
+
+// out[i] = number of cum entries < x[i] (numpy searchsorted side='left'),
+// parallel over queries; used by the synthetic generators' inverse-CDF draws.
+#include <algorithm>
+
+extern "C" int gcnb_searchsorted_f64(const double* cum, int64_t n, const double* x, int64_t k, int64_t* out) {
+  if (n < 0 || k < 0 || (k > 0 && (!cum || !x || !out))) return 1;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < k; ++i) out[i] = std::lower_bound(cum, cum + n, x[i]) - cum;
+  return 0;
+}

@@ -41,7 +41,7 @@ def build_host(force: bool = False) -> Path:
         HOST_LIB.parent.mkdir(exist_ok=True)
         cxx = "/usr/bin/g++" if Path("/usr/bin/g++").exists() else "g++"
         tmp = HOST_LIB.with_suffix(".so.tmp")
-        subprocess.run([cxx, "-O3", "-std=c++17", "-fPIC", "-shared", "-o", str(tmp), *map(str, HOST_SRCS)],
+        subprocess.run([cxx, "-O3", "-std=c++17", "-fPIC", "-shared", "-fopenmp", "-o", str(tmp), *map(str, HOST_SRCS)],
                        check=True)
         os.replace(tmp, HOST_LIB)
     return HOST_LIB
@@ -62,6 +62,8 @@ def _load():
         lib.gcnb_label_propagation.restype = ctypes.c_int
         lib.gcnb_csr_transpose.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp]
         lib.gcnb_csr_transpose.restype = ctypes.c_int
+        lib.gcnb_searchsorted_f64.argtypes = [vp, i64, vp, i64, vp]
+        lib.gcnb_searchsorted_f64.restype = ctypes.c_int
         _hlib = lib
     return _hlib
 

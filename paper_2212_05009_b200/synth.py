@@ -104,6 +104,23 @@ def roadnet(seed: int = 0, side: int = 1404, kept_edges: int = 2_766_607) -> Csr
     return _csr_from_pairs(n, np.concatenate([u, w]), np.concatenate([w, u]))
 
 
+def _searchsorted(cum: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """np.searchsorted(cum, x) (side='left'), threaded in csrc_host/csr.cpp when
+    the host library is built (identical results)."""
+    try:
+        from . import hp
+
+        lib = hp._load()
+    except (ImportError, OSError):
+        return np.searchsorted(cum, x)
+    cum = np.ascontiguousarray(cum, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty(len(x), dtype=np.int64)
+    if lib.gcnb_searchsorted_f64(cum.ctypes.data, len(cum), x.ctypes.data, len(x), out.ctypes.data) != 0:
+        raise ValueError("searchsorted: bad arguments")
+    return out
+
+
 def products(seed: int = 0, n: int = 2_449_029, pairs: int = 61_859_140, blocks: int = 2048,
              intra: float = 0.8, sigma: float = 1.0, block_offset: float = 16.0) -> CsrMatrix:
     rng = np.random.default_rng([seed, 0x9200])
@@ -113,11 +130,7 @@ def products(seed: int = 0, n: int = 2_449_029, pairs: int = 61_859_140, blocks:
     cum = np.cumsum(prop)
 
     def inv_cdf(x):
-        # sorted queries make the binary searches cache-friendly; the draws stay i.i.d.
-        order = np.argsort(x)
-        out = np.empty(len(x), dtype=np.int64)
-        out[order] = np.minimum(np.searchsorted(cum, x[order]), n - 1)
-        return out
+        return np.minimum(_searchsorted(cum, x), n - 1)
 
     def draw(k):
         u = inv_cdf(rng.random(k) * cum[-1])
