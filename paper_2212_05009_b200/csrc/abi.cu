@@ -2,7 +2,9 @@
 // device memory that can be mapped into peer processes (CUDA IPC), peer access.
 #include <cstdarg>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "common.cuh"
 
@@ -42,6 +44,46 @@ int num_sms() {
     g_sms[dev] = n;
   }
   return g_sms[dev];
+}
+
+// Zero-initialised at module load on every device; a kernel that takes a
+// slot leaves it zero when it finishes (see k_agg).
+constexpr int SCHED_SLOTS = 1024;
+__device__ int g_sched[2 * SCHED_SLOTS];
+
+int* sched_counter(cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, int> slot_of;
+  static int next_slot[MAX_DEVICES] = {0};
+  static int* base[MAX_DEVICES] = {nullptr};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAX_DEVICES) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  if (!base[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_sched) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    base[dev] = static_cast<int*>(p);
+  }
+  auto key = std::make_pair(dev, st);
+  auto it = slot_of.find(key);
+  int slot;
+  if (it != slot_of.end()) {
+    slot = it->second;
+  } else {
+    if (next_slot[dev] >= SCHED_SLOTS) {
+      set_error(GCNB_EINVAL, "more than %d streams used with dynamically scheduled kernels", SCHED_SLOTS);
+      return nullptr;
+    }
+    slot = next_slot[dev]++;
+    slot_of.emplace(key, slot);
+  }
+  return base[dev] + 2 * slot;
 }
 
 }  // namespace gcnb

@@ -22,6 +22,10 @@ extern std::atomic<uint64_t> g_launches;
 int set_error(int code, const char* fmt, ...);
 int cuda_fail(cudaError_t e, const char* what);
 int num_sms();
+// Work counter (2 ints, zero between launches) for dynamically scheduled
+// kernels launched on `st`: one slot per (device, stream), so kernels running
+// concurrently on different streams never share a counter.
+int* sched_counter(cudaStream_t st);
 
 // dense.cu: register-blocked SIMT transform for the wide dense layers
 bool dense_blocked_applies(int d_in, int d_out);
