@@ -284,14 +284,17 @@ def run_single(args):
 
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
+    log(f"building workload {args.workload}")
     wl = build_workload(args.workload, args.seed)
     n = wl["n"]
     owner = np.zeros(n, dtype=np.int64)
+    log("scatter")
     t_loc = time.perf_counter()
     states = gb.scatter(wl["a_hat"], wl["h0"], owner, wl["model"], directed=wl["directed"], p=1, device=dev,
                         locality=args.locality == "on")
     t_loc = time.perf_counter() - t_loc
     runner = EpochRunner(states, wl["labels"])
+    log("first (eager) epoch")
 
     c0 = _lib.launch_count()
     runner.enqueue()
@@ -304,6 +307,7 @@ def run_single(args):
     # two graphs of the same epoch: a plain one for the step time and one with
     # per-kernel event spans (event nodes between kernels cost ~µs each, so
     # they are kept out of the timed step)
+    log("warm-up done; capturing graphs")
     timer = profiling.KernelTimer()
     g_spans = g_plain = None
     if not args.no_graph:
@@ -315,6 +319,7 @@ def run_single(args):
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     torch.cuda.synchronize()
+    log("timed epochs")
     with ClockSampler(0) as clocks:
         for i in range(args.steps):
             flush.zero_()
@@ -339,6 +344,7 @@ def run_single(args):
         torch.cuda.synchronize()
         kernel_rows.extend(timer.results())
 
+    log("end-to-end epochs")
     # end to end through the public API: pinned host features -> device, one
     # train_epochs call (labels upload, forward, loss, backward, SGD, loss D2H)
     net = gb.DeviceNetwork(1)
@@ -360,6 +366,7 @@ def run_single(args):
 
     peak, peak_kind = measured_peaks()
     kname, achieved, kms, kbytes, table = roofline_summary(kernel_rows, peak, peak_kind, args.steps)
+    log("CPU baseline")
     cpu_times, cpu_threads = ([float("nan")], 0) if args.kernels_only else cpu_epoch_timer(wl)
     cpu_ms = 1e3 * float(np.mean(cpu_times))
     clk = clocks.summary()
@@ -390,6 +397,12 @@ def run_single(args):
 
 
 _OUT_FD = None
+_T0 = time.perf_counter()
+
+
+def log(msg: str) -> None:
+    """Progress on stderr (the JSON line alone goes to stdout)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
 def emit(line: dict) -> None:

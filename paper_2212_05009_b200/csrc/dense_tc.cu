@@ -1,24 +1,21 @@
-// Tensor-core (tcgen05) fp32-class dense transform Y[r] = act(X[r]·W) for the
-// wide layers (the `@ w` of runtime.py:299/304), 3xTF32:
+// Tensor-core (tcgen05) fp32-class dense transforms for the wide layers (the
+// `@ w` of runtime.py:299/304, `agg @ weights.T` and `h.T @ aggregated` of
+// runtime.py:353-356), 3xTF32:
 //
 //   x·w ≈ hi(x)·hi(w) + hi(x)·lo(w) + lo(x)·hi(w),  hi = tf32 truncation, lo = x − hi
 //
 // (relative error ~2^-21 per product, fp32 accumulation in TMEM; a single
 // TF32 product misses the 1e-4 bar, SURVEY key facts).  The tensor core reads
 // tf32 operands as fp32 bit patterns and ignores the low 13 mantissa bits, so
-// the raw fp32 tile *is* hi(x); lo(x) is written over the tile in place once
+// a raw fp32 tile *is* hi(x); lo(x) is written over the tile in place once
 // the hi MMAs have drained.
 //
-// One persistent CTA per SM (256 threads): W (K×N, fp32) is staged once as the
-// K-major B operand in both hi and lo form; 128-row X tiles are double
-// buffered with cp.async (tile i+1 streams in while tile i is multiplied), in
-// the canonical no-swizzle K-major layout (8-row × 16-byte core matrices).
-// Thread 0 issues the MMAs (M=128, N=round16(d_out), K=8 per instruction)
-// into a TMEM accumulator; completion is tracked with tcgen05.commit → an
-// mbarrier; all 8 warps drain the accumulator with tcgen05.ld (warp w reads
-// TMEM lanes 32·(w%4).., half the columns each), apply the activation and store.
+// k_dense_tc: Y[r] = act(X[r]·W) or (X[r]·Wᵀ) ⊙ σ'(H[r]) — warp-specialised,
+// persistent, MMA M = output features (see the kernel comment).
+// k_dw_tc:    per-CTA ΔW partials Σ_r H[r]ᵀ·A[r] with K = graph rows.
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 
 #include "common.cuh"
 
@@ -26,7 +23,6 @@ namespace gcnb {
 
 namespace {
 
-constexpr int TC_M = 128;        // rows per tile = MMA M = TMEM lanes
 constexpr int TC_THREADS = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -59,14 +55,28 @@ __device__ __forceinline__ void mma_commit(uint32_t mbar) {
                : "memory");
 }
 
+// Parity wait with a watchdog: a phase that never completes (a pipeline bug)
+// traps after ~4 s instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred done;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
-      "@!done bra WAIT_%=;\n\t}" ::"r"(mbar),
-      "r"(parity)
-      : "memory");
+  uint64_t t0 = 0;
+  for (;;) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(mbar), "r"(parity)
+        : "memory");
+    if (done) return;
+    uint64_t now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (t0 == 0) {
+      t0 = now;
+    } else if (now - t0 > 4000000000ull) {
+      printf("gcnb: mbarrier wait timed out (block %d thread %d bar 0x%x parity %u)\n", blockIdx.x, threadIdx.x,
+             mbar, parity);
+      __trap();
+    }
+  }
 }
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -85,29 +95,22 @@ __device__ __forceinline__ float tf32_lo(float x) {
   return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-// Byte offset of 16-byte chunk c of row r in a K-major canonical tile with
-// `nch` chunks per row: core matrix (r/8, c) is 128 contiguous bytes.
-__device__ __forceinline__ uint32_t kmaj_off(int r, int c, int nch) {
-  return (uint32_t)(((r >> 3) * nch + c) * 128 + (r & 7) * 16);
+// Byte offset of 16-byte chunk c (4 floats of K) of row r in a K-major
+// SWIZZLE_128B tile of `rows` rows: K runs in blocks of 32 floats (one 128-byte
+// line per row); a block is `rows` lines, 8-row atoms of 1024 bytes, and the
+// chunk's position inside its line is XOR-permuted by the row (r & 7).  The
+// tile base must be 1024-byte aligned.
+__device__ __forceinline__ uint32_t sw128_off(int r, int c, int rows) {
+  return (uint32_t)((c >> 3) * rows * 128 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
-// Stream one 128-row X tile into a stage: lanes map (row-in-group, chunk) so
-// a quarter-warp fills one 128-byte core matrix (bank-conflict free) and four
-// lanes of a row read 64 contiguous bytes.
-__device__ __forceinline__ void load_tile(uint32_t stage, const float* __restrict__ X, int ldx,
-                                          const int* __restrict__ rows, int n_rows, int m0, int kc, int nch) {
-  const int quads = (kc + 3) >> 2;
-  const int total = (TC_M / 8) * quads * 32;
-  for (int idx = threadIdx.x; idx < total; idx += TC_THREADS) {
-    const int rr = idx & 7, cc = (idx >> 3) & 3, gq = idx >> 5;
-    const int g = gq % (TC_M / 8), q = gq / (TC_M / 8);
-    const int r = g * 8 + rr, c = q * 4 + cc;
-    const int i = m0 + r;
-    const bool ok = c < kc && i < n_rows;
-    const int xr = ok ? (rows ? __ldg(rows + i) : i) : 0;
-    cp16(stage + kmaj_off(r, c, nch), X + (size_t)xr * ldx + 4 * c, ok);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
+// Descriptor of MMA K-step s (8 tf32 = 32 bytes) of a SWIZZLE_128B K-major
+// tile: the start advances 32 bytes inside the 128-byte line and a whole
+// block of `rows` lines every 4 steps; SBO = 1024 (next 8-row atom), LBO
+// unused (1), layout type 2 (SWIZZLE_128B) at bits [61,64).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t base, int s, int rows) {
+  const uint32_t addr = base + (uint32_t)((s >> 2) * rows * 128 + (s & 3) * 32);
+  return smem_desc(addr, 16, 1024) | (2ull << 61);
 }
 
 }  // namespace
@@ -116,53 +119,121 @@ namespace {
 int g_dense_mode = 0;  // 0 auto, 1 force SIMT, 2 force tensor core (where it applies)
 }
 
-__global__ void __launch_bounds__(TC_THREADS, 1)
+// Warp-specialised, transposed-orientation transform: the MMA computes
+// Dᵀ = Wᵀ·Xᵀ, i.e. M = 128 output features (TMEM lanes), N = NT_ rows of X per
+// tile (TMEM columns), K = d_in.  A = Wᵀ (hi and lo) lives in TENSOR memory for
+// the whole persistent CTA (columns [0, 2·Kp)), so shared memory holds only the
+// X stages (SWIZZLE_128B, 2-4 of them) and each MMA reads one operand from
+// shared memory.  With the features on TMEM lanes, the epilogue thread for
+// feature m holds consecutive rows, so a warp store writes 32 consecutive
+// features of one row (128 contiguous bytes).
+//   warps 0-7   epilogue: tcgen05.ld → act / ⊙σ'(mask) → coalesced stores
+//               (two warps per TMEM lane quarter, each half of the tile's rows);
+//               warps 0-3 also write Wᵀ hi/lo into TMEM at start
+//   warps 8-11  producer: cp.async X (and mask) tile → stage
+//   warps 12-15 converter: lo(x) in place once the stage's hi MMAs drained
+//   warp 16     TMEM owner; lane 0 issues the MMAs, software-pipelined as
+//               hi(t) · lo(t-1) so the tensor core runs while tile t converts
+// Accumulators: two buffers of NT_ columns at TMEM column 256.
+constexpr int DT_WARPS = 17;
+constexpr int DT_THREADS = DT_WARPS * 32;
+constexpr int DT_PROD = 128;  // producer threads (warps 8-11)
+constexpr int DT_CONV = 128;  // converter threads (warps 12-15)
+constexpr int DT_EPI = 256;   // epilogue threads (warps 0-7)
+constexpr int DT_MAX_STAGES = 4;
+
+namespace {
+
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+}
+
+// D (tmem) (+)= A (tmem) · B (smem descriptor), kind::tf32
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// X rows [m0, m0+N) (through the row list) into a K-major SWIZZLE_128B tile.
+__device__ __forceinline__ void load_x_rows(uint32_t stage, const float* __restrict__ X, int ldx,
+                                            const int* __restrict__ rows, int n_rows, int m0, int N, int kc, int tid) {
+  for (int idx = tid; idx < N * kc; idx += DT_PROD) {
+    const int r = idx / kc, c = idx - r * kc;   // a row's chunks are consecutive lanes (coalesced)
+    const int i = m0 + r;
+    const bool ok = i < n_rows;
+    const int xr = ok ? (rows ? __ldg(rows + i) : i) : 0;
+    cp16(stage + sw128_off(r, c, N), X + (size_t)xr * ldx + 4 * c, ok);
+  }
+}
+
+// Mask rows (H_prev of the backward epilogue) into a row-major [N][mpad] tile.
+__device__ __forceinline__ void load_mask_rows(uint32_t stage, const float* __restrict__ Hm, int ldhm,
+                                               const int* __restrict__ rows, int n_rows, int m0, int N, int mpad,
+                                               int tid) {
+  const int c4 = mpad / 4;
+  for (int idx = tid; idx < N * c4; idx += DT_PROD) {
+    const int r = idx / c4, c = idx - r * c4;
+    const int i = m0 + r;
+    const bool ok = i < n_rows;
+    const int hr = ok ? (rows ? __ldg(rows + i) : i) : 0;
+    cp16(stage + (uint32_t)(r * mpad + 4 * c) * 4, Hm + (size_t)hr * ldhm + 4 * c, ok);
+  }
+}
+
+}  // namespace
+
+template <bool RELU, bool MASKED>
+__global__ void __launch_bounds__(DT_THREADS, 1)
     k_dense_tc(const float* __restrict__ X, int ldx, const int* __restrict__ rows, int n_rows, int K,
-               const float* __restrict__ W, int ldw, int w_nk, int N, float* __restrict__ Y, int ldy, int act,
-               const float* __restrict__ Hm, int ldhm) {
+               const float* __restrict__ W, int ldw, int w_nk, int M, int NT_, int S, float* __restrict__ Y,
+               int ldy, const float* __restrict__ Hm, int ldhm) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t bars[4 * DT_MAX_STAGES + 4];
   __shared__ uint32_t tmem_base_slot;
-  const int Kp = (K + 7) & ~7, nch = Kp / 4, kc = (K + 3) / 4;  // chunks per row (padded / valid)
-  const int Np = (N + 15) & ~15;
-  const uint32_t tile_bytes = TC_M * Kp * 4, b_bytes = Np * Kp * 4;
-  uint8_t* a_stage[2] = {smem, smem + tile_bytes};
-  uint8_t* b_hi = smem + 2 * tile_bytes;
-  uint8_t* b_lo = b_hi + b_bytes;
+  const int Kp = (K + 7) & ~7, kc = (K + 3) / 4;  // MMA K extent, loaded chunks per row
+  const int Kb = (K + 31) & ~31;                  // smem K extent (whole 128-byte swizzle lines)
+  const int mpad = (M + 3) & ~3;                  // mask tile row stride (floats)
+  const uint32_t x_bytes = (uint32_t)NT_ * Kb * 4;
+  const uint32_t m_bytes = MASKED ? (uint32_t)NT_ * mpad * 4 : 0;
+  const uint32_t st_bytes = (x_bytes + m_bytes + 1023) & ~1023u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles = (n_rows + TC_M - 1) / TC_M;
-  const uint32_t tmem_cols = Np <= 32 ? 32 : Np <= 64 ? 64 : Np <= 128 ? 128 : 256;
+  const int n_tiles = (n_rows + NT_ - 1) / NT_;
+  // barriers: full[S] hi_done[S] lo_ready[S] empty[S] | acc_full[2] acc_empty[2]
+  auto bar = [&](int kind, int i) { return smem_u32(&bars[kind * DT_MAX_STAGES + i]); };
+  auto abar = [&](int kind, int i) { return smem_u32(&bars[4 * DT_MAX_STAGES + 2 * kind + i]); };
+  if (smem_u32(smem) & 1023u) __trap();           // swizzle atoms need 1024-byte alignment
 
-  // first tile in flight before the one-time setup
-  if ((int)blockIdx.x < n_tiles) load_tile(smem_u32(a_stage[0]), X, ldx, rows, n_rows, blockIdx.x * TC_M, kc, nch);
-
-  // zero the K pad chunks of both stages (never written by the loads)
-  for (int idx = threadIdx.x; idx < 2 * TC_M * (nch - kc); idx += TC_THREADS) {
-    const int s = idx / (TC_M * (nch - kc)), rem = idx % (TC_M * (nch - kc));
-    const int r = rem % TC_M, c = kc + rem / TC_M;
-    *reinterpret_cast<float4*>(a_stage[s] + kmaj_off(r, c, nch)) = make_float4(0.f, 0.f, 0.f, 0.f);
+  // K pad chunks of every X stage are never loaded: zero them once
+  const int pad_ch = Kp / 4 - kc;
+  for (int idx = threadIdx.x; idx < S * NT_ * pad_ch; idx += DT_THREADS) {
+    const int sidx = idx / (NT_ * pad_ch), rem = idx % (NT_ * pad_ch);
+    const int r = rem % NT_, c = kc + rem / NT_;
+    *reinterpret_cast<float4*>(smem + sidx * st_bytes + sw128_off(r, c, NT_)) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  // B operand = Wᵀ (N rows × Kp, K-major): element (n, k) = W[k][n]; pad rows/cols zero
-  for (int idx = threadIdx.x; idx < Np * nch; idx += TC_THREADS) {
-    const int n = idx % Np, c = idx / Np;
-    float v[4], l[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int k = 4 * c + e;
-      v[e] = (n < N && k < K) ? __ldg(W + (w_nk ? (size_t)n * ldw + k : (size_t)k * ldw + n)) : 0.0f;
-      l[e] = tf32_lo(v[e]);
-    }
-    *reinterpret_cast<float4*>(b_hi + kmaj_off(n, c, nch)) = make_float4(v[0], v[1], v[2], v[3]);
-    *reinterpret_cast<float4*>(b_lo + kmaj_off(n, c, nch)) = make_float4(l[0], l[1], l[2], l[3]);
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_slot)),
-                 "r"(tmem_cols)
+  if (warp == 16) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)) : "memory");
+    for (int i = 0; i < S; ++i) {
+      mbar_init(bar(0, i), DT_PROD);
+      mbar_init(bar(1, i), 1);
+      mbar_init(bar(2, i), DT_CONV);
+      mbar_init(bar(3, i), MASKED ? 1 + DT_EPI : 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(abar(0, i), 1);
+      mbar_init(abar(1, i), DT_EPI);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   fence_async_smem();
@@ -170,103 +241,202 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_after_sync();
   const uint32_t tmem = tmem_base_slot;
-  const uint32_t mb = smem_u32(&mbar);
-  const uint32_t idesc = idesc_tf32(TC_M, Np);
-  const uint32_t sbo_a = nch * 128, sbo_b = nch * 128;
-  uint32_t phase = 0;
+  const uint32_t acc0 = tmem + 256;
 
-  int it = 0;
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
-    const int next = tile + gridDim.x;
-    if (next < n_tiles) {
-      load_tile(smem_u32(a_stage[(it + 1) & 1]), X, ldx, rows, n_rows, next * TC_M, kc, nch);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    fence_async_smem();
-    __syncthreads();
-    uint8_t* a = a_stage[it & 1];
-    const uint32_t a_addr = smem_u32(a), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
-    // hi(x)·hi(w) + hi(x)·lo(w)
-    if (threadIdx.x == 0) {
-      tc_after_sync();
-      for (int s = 0; s < Kp / 8; ++s) {
-        const uint64_t da = smem_desc(a_addr + s * 256, 128, sbo_a);
-        mma_tf32(tmem, da, smem_desc(bh + s * 256, 128, sbo_b), idesc, s > 0);
-        mma_tf32(tmem, da, smem_desc(bl + s * 256, 128, sbo_b), idesc, 1);
+  if (warp < 4) {
+    // Wᵀ hi → columns [0, Kp), lo → [Kp, 2Kp): lane m = output feature, column k.
+    // Element (m, k) = W[k][m] (w_nk: W[m][k]); pad features / K zero.
+    const int m = warp * 32 + lane;
+    for (int c0 = 0; c0 < Kp; c0 += 8) {
+      uint32_t hi[8], lo[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int k = c0 + e;
+        const float v = (m < M && k < K) ? __ldg(W + (w_nk ? (size_t)m * ldw + k : (size_t)k * ldw + m)) : 0.0f;
+        hi[e] = __float_as_uint(v);
+        lo[e] = __float_as_uint(tf32_lo(v));
       }
-      mma_commit(mb);
+      const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "r"(hi[0]),
+                   "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7])
+                   : "memory");
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta + Kp),
+                   "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7])
+                   : "memory");
     }
-    mbar_wait(mb, phase);
-    phase ^= 1;
-    // lo(x) in place, then + lo(x)·hi(w)
-    for (int idx = threadIdx.x; idx < TC_M * kc; idx += TC_THREADS) {
-      const int r = idx % TC_M, c = idx / TC_M;
-      float4* p = reinterpret_cast<float4*>(a + kmaj_off(r, c, nch));
-      const float4 v = *p;
-      *p = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+
+  if (warp >= 8 && warp < 12) {
+    // ---------------- producer
+    const int tid = threadIdx.x - 256;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+      const int s = t % S;
+      if (t >= S) mbar_wait(bar(3, s), (uint32_t)(t / S - 1) & 1u);
+      const uint32_t st = smem_u32(smem + s * st_bytes);
+      load_x_rows(st, X, ldx, rows, n_rows, tile * NT_, NT_, kc, tid);
+      if (MASKED) load_mask_rows(st + x_bytes, Hm, ldhm, rows, n_rows, tile * NT_, NT_, mpad, tid);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (t >= 1) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        fence_async_smem();
+        mbar_arrive(bar(0, (t - 1) % S));
+      }
     }
-    fence_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    if (t >= 1) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_async_smem();
+      mbar_arrive(bar(0, (t - 1) % S));
+    }
+  } else if (warp >= 12 && warp < 16) {
+    // ---------------- lo(x) converter
+    const int tid = threadIdx.x - 384;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+      const int s = t % S;
+      const uint32_t par = (uint32_t)(t / S) & 1u;
+      mbar_wait(bar(0, s), par);  // every producer's copies visible
+      mbar_wait(bar(1, s), par);  // hi MMAs have read the tile
+      uint8_t* xs = smem + s * st_bytes;
+      for (int idx = tid; idx < NT_ * kc; idx += DT_CONV) {
+        const int r = idx % NT_, c = idx / NT_;
+        float4* q = reinterpret_cast<float4*>(xs + sw128_off(r, c, NT_));
+        const float4 v = *q;
+        *q = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+      }
+      fence_async_smem();
+      mbar_arrive(bar(2, s));
+    }
+  } else if (warp == 16) {
+    // ---------------- MMA issuer: hi(t) then lo(t-1)
+    if (lane == 0) {
+      const uint32_t idesc = idesc_tf32(128, NT_);
+      const int ksteps = Kp / 8;
+      int t = 0;
+      for (int tile = blockIdx.x;; tile += gridDim.x, ++t) {
+        const bool live = tile < n_tiles;
+        if (live) {
+          const int s = t % S, b = t & 1;
+          const uint32_t xs = smem_u32(smem + s * st_bytes);
+          mbar_wait(bar(0, s), (uint32_t)(t / S) & 1u);
+          if (t >= 2) mbar_wait(abar(1, b), (uint32_t)((t >> 1) - 1) & 1u);
+          tc_after_sync();
+          const uint32_t d = acc0 + (uint32_t)(b * NT_);
+          for (int k = 0; k < ksteps; ++k) {
+            const uint64_t db = sw128_desc(xs, k, NT_);
+            mma_tf32_ts(d, tmem + 8 * k, db, idesc, k > 0);
+            mma_tf32_ts(d, tmem + Kp + 8 * k, db, idesc, 1);
+          }
+          mma_commit(bar(1, s));
+        }
+        if (t >= 1) {
+          const int tp = t - 1, sp = tp % S, bp = tp & 1;
+          const uint32_t xs = smem_u32(smem + sp * st_bytes);
+          mbar_wait(bar(2, sp), (uint32_t)(tp / S) & 1u);
+          tc_after_sync();
+          const uint32_t d = acc0 + (uint32_t)(bp * NT_);
+          for (int k = 0; k < ksteps; ++k) mma_tf32_ts(d, tmem + 8 * k, sw128_desc(xs, k, NT_), idesc, 1);
+          mma_commit(bar(3, sp));
+          mma_commit(abar(0, bp));
+        }
+        if (!live) break;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue: warp e drains TMEM lanes 32(e%4).. (features),
+    // columns (tile rows) of its half e/4 of the tile
+    const int q = warp & 3, hs = warp >> 2;
+    const int span = NT_ / 2;
+    const int m = q * 32 + lane;
+    const bool m_out = m < ldy, m_mask = m < mpad;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+      const int s = t % S, b = t & 1;
+      mbar_wait(abar(0, b), (uint32_t)(t >> 1) & 1u);
+      if (MASKED) mbar_wait(bar(0, s), (uint32_t)(t / S) & 1u);
       tc_after_sync();
-      for (int s = 0; s < Kp / 8; ++s)
-        mma_tf32(tmem, smem_desc(a_addr + s * 256, 128, sbo_a), smem_desc(bh + s * 256, 128, sbo_b), idesc, 1);
-      mma_commit(mb);
-    }
-    mbar_wait(mb, phase);
-    phase ^= 1;
-    tc_after_sync();
-    // epilogue: warp w drains TMEM lanes 32(w%4).. (rows), columns [half·Np/2, (half+1)·Np/2)
-    {
-      const int quarter = warp & 3, half = warp >> 2;
-      const int r = quarter * 32 + lane;
-      const int i = tile * TC_M + r;
-      const bool ok = i < n_rows;
-      const int yr = ok ? (rows ? __ldg(rows + i) : i) : 0;
-      const int c_lo = half * (Np / 2), c_hi = c_lo + Np / 2;
-      for (int c0 = c_lo; c0 < c_hi; c0 += 8) {
-        uint32_t v[8];
-        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
+      const float* ms = reinterpret_cast<const float*>(smem + s * st_bytes + x_bytes);
+      const int i0 = tile * NT_;
+      for (int n0 = hs * span; n0 < (hs + 1) * span && i0 + n0 < n_rows; n0 += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = acc0 + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NT_ + n0);
         asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (ok) {
-          float* y = Y + (size_t)yr * ldy + c0;
+        float o[16];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (c0 + 4 * h < ldy) {
-              float4 o = make_float4(__uint_as_float(v[4 * h]), __uint_as_float(v[4 * h + 1]),
-                                     __uint_as_float(v[4 * h + 2]), __uint_as_float(v[4 * h + 3]));
-              if (Hm) {  // backward: (agg·Wᵀ) ⊙ σ'(H_prev), σ' from h (gcn.py:101-104)
-                const float4 hv = __ldg(reinterpret_cast<const float4*>(Hm + (size_t)yr * ldhm + c0) + h);
-                o.x *= act_grad_from_h(hv.x, act);
-                o.y *= act_grad_from_h(hv.y, act);
-                o.z *= act_grad_from_h(hv.z, act);
-                o.w *= act_grad_from_h(hv.w, act);
-              } else {
-                o = act_fwd4(o, act);
-              }
-              reinterpret_cast<float4*>(y)[h] = o;
-            }
+        for (int j = 0; j < 16; ++j) {
+          o[j] = __uint_as_float(v[j]);
+          if (MASKED) {
+            const float hv = m_mask ? ms[(n0 + j) * mpad + m] : 1.0f;
+            o[j] = RELU ? (hv > 0.0f ? o[j] : 0.0f) : o[j];
+          } else if (RELU) {
+            o[j] = fmaxf(o[j], 0.0f);
+          }
+        }
+        if (!m_out) continue;
+        if (rows == nullptr && i0 + n0 + 16 <= n_rows) {
+          float* p = Y + (size_t)(i0 + n0) * ldy + m;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) p[(size_t)j * ldy] = o[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int i = i0 + n0 + j;
+            if (i < n_rows) Y[(size_t)(rows ? __ldg(rows + i) : i) * ldy + m] = o[j];
           }
         }
       }
+      tc_before_sync();
+      mbar_arrive(abar(1, b));
+      if (MASKED) mbar_arrive(bar(3, s));
     }
-    tc_before_sync();
-    __syncthreads();  // TMEM drained and stage (it & 1) free before they are reused
   }
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  if (warp == 16) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
+
+namespace {
+constexpr size_t DT_SMEM_MAX = 227 * 1024 - 1024;
+
+// Rows per tile (MMA N) and stage count: the largest tile of 128/64/32 rows
+// for which at least three stages fit (up to DT_MAX_STAGES).  Three is the
+// minimum: the producer signals tile t-1 only after it has waited for the
+// stage of tile t to drain (lo MMAs of tile t-S), while the MMA issuer needs
+// tile t-1 before it issues those lo MMAs of tile t-2 — with S = 2 that is a
+// cycle.
+int dense_tc_tile(int d_in, int d_out, bool masked, int* stages, size_t* smem_out) {
+  if (d_in > 128 || d_out > 128) return 0;  // Wᵀ hi+lo ≤ 256 TMEM columns; one 128-lane half
+  const int Kb = (d_in + 31) & ~31, mpad = (d_out + 3) & ~3;
+  for (int nt = 128; nt >= 32; nt >>= 1) {
+    const size_t st = ((size_t)nt * (Kb + (masked ? mpad : 0)) * 4 + 1023) & ~(size_t)1023;
+    const int s = (int)std::min<size_t>(DT_MAX_STAGES, DT_SMEM_MAX / st);
+    if (s >= 3) {
+      *stages = s;
+      *smem_out = s * st;
+      return nt;
+    }
+  }
+  return 0;
+}
+}  // namespace
 
 bool dense_tc_applies(int d_in, int d_out) {
   if (g_dense_mode == 1) return false;
-  const int Kp = (d_in + 7) & ~7, Np = (d_out + 15) & ~15;
-  const size_t smem = (size_t)2 * TC_M * Kp * 4 + (size_t)2 * Np * Kp * 4;
-  const bool fits = d_in <= 256 && d_out <= 256 && smem <= 220 * 1024;
+  int stages = 0;
+  size_t smem = 0;
+  // the backward form carries a mask tile: require that it fits too
+  const bool fits = dense_tc_tile(d_in, d_out, true, &stages, &smem) > 0;
   if (g_dense_mode == 2) return fits;
   return fits && d_in >= 32 && d_out >= 32;
 }
@@ -274,13 +444,19 @@ bool dense_tc_applies(int d_in, int d_out) {
 int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
                     float* y, int ldy, int act, cudaStream_t st, const float* w_nk, int ld_wnk, const float* hmask,
                     int ldhm) {
-  const int Kp = (d_in + 7) & ~7, Np = (d_out + 15) & ~15;
-  const size_t smem = (size_t)2 * TC_M * Kp * 4 + (size_t)2 * Np * Kp * 4;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_dense_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int tiles = (n_rows + TC_M - 1) / TC_M;
+  int stages = 0;
+  size_t smem = 0;
+  const int nt = dense_tc_tile(d_in, d_out, hmask != nullptr, &stages, &smem);
+  GCNB_REQUIRE(nt > 0, "dense (tcgen05): widths %d -> %d not supported", d_in, d_out);
+  GCNB_REQUIRE(!hmask || ldhm >= ((d_out + 3) & ~3), "dense (tcgen05): mask stride too small");
+  const bool relu = act == GCNB_ACT_RELU;
+  auto fn = hmask ? (relu ? k_dense_tc<true, true> : k_dense_tc<false, true>)
+                  : (relu ? k_dense_tc<true, false> : k_dense_tc<false, false>);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int tiles = (n_rows + nt - 1) / nt;
   const int grid = std::max(1, std::min(tiles, num_sms()));
-  k_dense_tc<<<grid, TC_THREADS, smem, st>>>(x, ldx, rows, n_rows, d_in, w_nk ? w_nk : w, w_nk ? ld_wnk : round4(d_out),
-                                             w_nk ? 1 : 0, d_out, y, ldy, act, hmask, ldhm);
+  fn<<<grid, DT_THREADS, smem, st>>>(x, ldx, rows, n_rows, d_in, w_nk ? w_nk : w, w_nk ? ld_wnk : round4(d_out),
+                                     w_nk ? 1 : 0, d_out, nt, stages, y, ldy, hmask, ldhm);
   GCNB_AFTER_LAUNCH("dense (tcgen05 3xTF32)");
   return GCNB_OK;
 }

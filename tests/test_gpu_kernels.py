@@ -243,10 +243,10 @@ def test_bwd_split_equals_fused_bitwise(d_p, d_k, dense_mode):
 
 @pytest.mark.parametrize("d_p,d_k", [(100, 128), (128, 47)])
 def test_bwd_tcgen05_many_tiles(d_p, d_k):
-    """Split backward on the tcgen05 epilogue over many 64-row ΔW tiles per CTA and
+    """Split backward on the tcgen05 epilogue over many tiles per CTA (every stage reused) and
     a ragged tail: G_prev and ΔW within TOL of the oracle, ΔW deterministic,
     and SIMT and tcgen05 engines agree within TOL."""
-    n = 64 * 148 * 3 + 29
+    n = 128 * 148 * 5 + 29  # several tiles per CTA in every stage of both engines
     rng = np.random.default_rng(21)
     a = rand_csr(n, n, 6.0 / n, 22)
     g = rng.standard_normal((n, d_k))
