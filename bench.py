@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--overlap", default="auto", choices=("auto", "on", "off"),
                     help="N>1: split layers into interior/boundary rows to hide the halo exchange "
                          "(auto: only when a rank's largest incoming halo exceeds 4 MiB)")
+    ap.add_argument("--reuse-fwd-aggregate", dest="reuse_fwd_aggregate", default="on", choices=("on", "off"),
+                    help="ΔW¹ = (Â·H⁰)ᵀ·G¹ from the forward's aggregate (exact reassociation of the reference's "
+                         "H⁰ᵀ·(Âᵀ·G¹)): no layer-1 backward aggregation or halo exchange")
     ap.add_argument("--kernels-only", action="store_true",
                     help="skip the e2e and CPU-baseline legs (for ncu launch lists)")
     return ap.parse_args()
@@ -291,7 +294,7 @@ def run_single(args):
     log("scatter")
     t_loc = time.perf_counter()
     states = gb.scatter(wl["a_hat"], wl["h0"], owner, wl["model"], directed=wl["directed"], p=1, device=dev,
-                        locality=args.locality == "on")
+                        locality=args.locality == "on", reuse_fwd_aggregate=args.reuse_fwd_aggregate == "on")
     t_loc = time.perf_counter() - t_loc
     runner = EpochRunner(states, wl["labels"])
     log("first (eager) epoch")
@@ -377,6 +380,7 @@ def run_single(args):
         "config": {"workload": wl["name"], "n": n, "nnz_ahat": wl["nnz"], "dims": list(wl["dims"]),
                    "directed": wl["directed"], "partition": "p=1", "locality": args.locality,
                    "scatter_s": round(t_loc, 2), "l2": "flushed (512 MiB write) before every step",
+                   "reuse_fwd_aggregate": states[0].dw1_from_fwd,
                    "graph": not args.no_graph, "seed": args.seed},
         "e2e": {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "loss_last": m[0].loss if m[0] is not None else None},

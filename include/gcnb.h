@@ -149,6 +149,15 @@ int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* 
                        const float* h_prev, int32_t ldhp, int32_t d_prev,
                        const float* w, float* g_prev, int32_t ldgp, int32_t act,
                        float* dw_partials, float* workspace, void* stream);
+/* ΔW partials alone: ΔW_part += X[r]^T · A[r] over the row list (no
+ * aggregation) — the `h.T @ aggregated` of runtime.py:355 when `aggregated`
+ * is already resident.  The runtime uses it for the first layer with
+ * X = Â·H^0 (the forward's aggregate) and A = G^1:
+ * (Â·H^0)^T·G^1 = H^0^T·(Â^T·G^1), so that layer needs no backward aggregation
+ * and no backward halo exchange.  Writes gcnb_bwd_grid(n_rows, d_prev, d_k, 0)
+ * partial blocks (d_prev*ld_k floats each) like gcnb_bwd_layer_f32. */
+int gcnb_dw_f32(const float* x, int32_t ldx, int32_t d_prev, const float* a, int32_t lda, int32_t d_k,
+                const int32_t* rows, int32_t n_rows, float* dw_partials, void* stream);
 /* Row stride (floats) of the optional `workspace` of gcnb_bwd_layer_f32 for
  * these widths, or 0 when the fused single-kernel form is always used.  With a
  * workspace of (own rows) × ld floats, large-ΔW layers run as an aggregation

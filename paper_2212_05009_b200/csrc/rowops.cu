@@ -866,6 +866,26 @@ extern "C" int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
   return GCNB_OK;
 }
 
+extern "C" int gcnb_dw_f32(const float* x, int32_t ldx, int32_t d_prev, const float* a, int32_t lda, int32_t d_k,
+                           const int32_t* rows, int32_t n_rows, float* dw_partials, void* stream) {
+  GCNB_REQUIRE(n_rows >= 0, "dw: n_rows must be >= 0");
+  GCNB_REQUIRE(d_prev >= 1 && d_prev <= 256 && d_k >= 1 && d_k <= 256, "dw: widths out of range");
+  GCNB_REQUIRE(ldx % 4 == 0 && lda % 4 == 0 && ldx >= round4(d_prev) && lda >= round4(d_k),
+               "dw: row strides must be multiples of 4 and cover the widths");
+  GCNB_REQUIRE(x && a && dw_partials && aligned16(x) && aligned16(a) && aligned16(dw_partials),
+               "dw: operands must be non-null and 16-byte aligned");
+  BwdPlan plan;
+  if (int rc = bwd_plan(n_rows, d_prev, d_k, false, &plan)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dw_tc_applies(d_prev, d_k))
+    return launch_dw_tc(x, ldx, d_prev, a, lda, d_k, rows, n_rows, dw_partials, plan.grid, st);
+  // SIMT: the backward kernel without CSR reads A's rows directly as its aggregated tile
+  plan.fn<<<plan.grid, NT, plan.smem, st>>>(nullptr, nullptr, nullptr, rows, n_rows, a, lda, d_k, x, ldx, d_prev,
+                                            nullptr, nullptr, 0, GCNB_ACT_IDENTITY, dw_partials, plan.T);
+  GCNB_AFTER_LAUNCH("dw");
+  return GCNB_OK;
+}
+
 extern "C" int gcnb_bwd_workspace_ld(int32_t d_prev, int32_t d_k, int32_t* ld_out) {
   GCNB_REQUIRE(ld_out != nullptr, "bwd workspace: null output");
   GCNB_REQUIRE(d_prev >= 1 && d_prev <= 256 && d_k >= 1 && d_k <= 256, "bwd workspace: widths out of range");

@@ -94,8 +94,11 @@ def arena_layout(n_own: int, r_fwd: int, r_bwd: int, dims, transform_first, p: i
 class RankSchedule:
     """Who sends to / waits for whom in every exchange of an epoch."""
 
-    def __init__(self, plan_fwd, plan_bwd, rank: int, n_layers: int):
+    def __init__(self, plan_fwd, plan_bwd, rank: int, n_layers: int, skip_bwd1: bool = False):
+        """skip_bwd1: the layer-1 backward exchange is not made (ΔW¹ from the
+        forward aggregate, runtime.ProcState reuse_fwd_aggregate)."""
         self.rank = rank
+        self.skip_bwd1 = skip_bwd1
         self.p = plan_fwd.p
         self.L = n_layers
         self.fwd_dst = [n for n in range(self.p) if n != rank and len(plan_fwd.send[rank][n])]
@@ -106,7 +109,8 @@ class RankSchedule:
     def exchanges(self):
         """[(phase, layer, dsts, srcs)] in epoch order (fwd k=1..L, bwd k=L..1)."""
         out = [("fwd", k, self.fwd_dst, self.fwd_src) for k in range(1, self.L + 1)]
-        out += [("bwd", k, self.bwd_dst, self.bwd_src) for k in range(self.L, 0, -1)]
+        out += [("bwd", k, self.bwd_dst, self.bwd_src) for k in range(self.L, 0, -1)
+                if not (k == 1 and self.skip_bwd1)]
         return out
 
     def doorbells_rung(self):
@@ -137,13 +141,14 @@ def build_rank(a_hat, owner, p: int, rank: int, directed: bool, row_labels=None)
     return plan_fwd, plan_bwd, layout
 
 
-def halo_bytes_per_epoch(layout, dims, transform_first) -> int:
+def halo_bytes_per_epoch(layout, dims, transform_first, skip_bwd1: bool = False) -> int:
     """Bytes this rank stores into peers per epoch (fwd + bwd exchanges)."""
     fw, bw = widths(dims, transform_first)
     L = len(dims) - 1
     rf = int(layout.fwd.send_ptr[-1]) if len(layout.fwd.send_ptr) else 0
     rb = int(layout.bwd.send_ptr[-1]) if len(layout.bwd.send_ptr) else 0
-    return sum(4 * ld_of(fw[k]) * rf + 4 * ld_of(bw[k]) * rb for k in range(1, L + 1))
+    return sum(4 * ld_of(fw[k]) * rf + (0 if k == 1 and skip_bwd1 else 4 * ld_of(bw[k]) * rb)
+               for k in range(1, L + 1))
 
 
 def reference_words_per_epoch(layout, dims) -> int:
@@ -210,12 +215,14 @@ class DistributedTrainer:
     OVERLAP_MIN_BYTES = 4 << 20
 
     def __init__(self, a_hat, h0, owner, p: int, model, labels, directed: bool, device, timeout_ms: int = 20000,
-                 row_labels=None, overlap: bool | None = None):
+                 row_labels=None, overlap: bool | None = None, reuse_fwd_aggregate: bool = False):
         """row_labels: optional per-vertex community labels for the locality
         layout of own rows (locality.py); None keeps ascending global ids.
         overlap: split each layer into interior rows (computed while the halo
         is in flight) and boundary rows; None = only when this rank's largest
-        incoming halo exceeds OVERLAP_MIN_BYTES."""
+        incoming halo exceeds OVERLAP_MIN_BYTES.
+        reuse_fwd_aggregate: ΔW¹ from the forward's Â·H⁰ (runtime.ProcState);
+        drops the layer-1 backward aggregation and exchange."""
         import torch
         import torch.distributed as dist
 
@@ -244,7 +251,8 @@ class DistributedTrainer:
         torch.cuda.set_device(device)
         self.arena = Arena(self.off, device)
         self.st = ProcState(layout, plan_fwd, plan_bwd, model, np.asarray(h0)[layout.global_rows], device,
-                            alloc=self.arena.rows_alloc)
+                            alloc=self.arena.rows_alloc, reuse_fwd_aggregate=reuse_fwd_aggregate)
+        self.sched.skip_bwd1 = self.st.skips_bwd_exchange(1)
         assert self.st.transform_first == tf and self.st.n_pack == n_pack
         self.n_lab = len(labels)
         self.st.set_labels(labels)
@@ -313,6 +321,9 @@ class DistributedTrainer:
             st.fwd_compute(k, "boundary" if self.overlap else "all")
         st.loss_grad(1.0 / self.n_lab)
         for k in range(L, 0, -1):
+            if st.skips_bwd_exchange(k):
+                st.reduce_dw(k, st.dw_from_forward(k))
+                continue
             if comm:
                 st.pack_to("bwd", k, self.bwd_bases[k], flags=self.halo_flag_bwd, counter=cnt)
             if self.overlap:
@@ -445,7 +456,8 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
     t_part = time.perf_counter() - t0
     ov = {"auto": None, "on": True, "off": False}[getattr(args, "overlap", "auto")]
     tr = DistributedTrainer(wl["a_hat"], wl["h0"], owner, world, wl["model"], wl["labels"], wl["directed"],
-                            device, row_labels=row_labels, overlap=ov)
+                            device, row_labels=row_labels, overlap=ov,
+                            reuse_fwd_aggregate=getattr(args, "reuse_fwd_aggregate", "on") == "on")
     st = tr.st
     from . import _lib as L_
 
@@ -525,7 +537,7 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
     e2e_ms = 1e3 * float(np.mean(e2e)) if e2e else float("nan")
     vals = torch.tensor([ms_rank, ms_compute, e2e_ms], dtype=torch.float64)
     dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    halo = torch.tensor([halo_bytes_per_epoch(tr.layout, st.dims, st.transform_first),
+    halo = torch.tensor([halo_bytes_per_epoch(tr.layout, st.dims, st.transform_first, st.skips_bwd_exchange(1)),
                          reference_words_per_epoch(tr.layout, st.dims)], dtype=torch.float64)
     dist.all_reduce(halo, op=dist.ReduceOp.SUM)
     peak, peak_kind = measured_peaks()
@@ -555,7 +567,7 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
                    "locality": args.locality,
                    "l2": "flushed (512 MiB write) before every step", "graph": True, "seed": args.seed,
                    "transport": "NVLink peer stores + doorbells (CUDA IPC), P2P allreduce",
-                   "overlap": tr.overlap},
+                   "overlap": tr.overlap, "reuse_fwd_aggregate": st.dw1_from_fwd},
         "e2e": {"value": round(e2e_max, 4), "unit": UNIT,
                 "h2d_bytes_per_step": int(h0_pinned.numel() * 4), "d2h_bytes_per_step": 8},
         "gpu_launches": int(launches * args.steps),

@@ -208,9 +208,16 @@ class ProcState:
     """
 
     def __init__(self, layout: RankLayout, plan_fwd: CommPlan, plan_bwd: CommPlan, model, h0: np.ndarray, dev,
-                 alloc=None):
+                 alloc=None, reuse_fwd_aggregate: bool = False):
         """`alloc(name, rows, width)` places the peer-written [own | halo] blocks
-        (default: private device memory; distributed.py passes an IPC arena)."""
+        (default: private device memory; distributed.py passes an IPC arena).
+
+        reuse_fwd_aggregate: compute ΔW¹ as (Â·H⁰)ᵀ·G¹ from the forward's
+        aggregate (kept in the layer-1 workspace) instead of H⁰ᵀ·(Âᵀ·G¹)
+        (runtime.py:346-356): the same product reassociated, so the first
+        layer's backward needs neither the aggregation of G¹ nor its halo
+        exchange.  Applies when layer 1 aggregates first through a workspace
+        (wide layers); the message log then lists only the exchanges made."""
         if alloc is None:
             def alloc(name, rows, width):
                 return devmem.empty_rows(rows, width, dev, ld=devmem.feat_ld(width))
@@ -286,6 +293,7 @@ class ProcState:
                 if not self.transform_first[k] and self.dims[k - 1] * devmem.ld_of(self.dims[k]) > 2048:
                     self.fwd_ws[k] = torch.zeros((max(n, 1), devmem.ld_of(self.dims[k - 1])), dtype=torch.float32,
                                                  device=dev)
+            self.dw1_from_fwd = bool(reuse_fwd_aggregate and L >= 1 and self.fwd_ws[1] is not None)
             # split-mode workspace (agg rows) for large-ΔW layers (gcnb_bwd_workspace_ld)
             self.bwd_ws = [None] * (L + 1)
             for k in range(1, L + 1):
@@ -473,6 +481,24 @@ class ProcState:
                       0 if self.bwd_ws[k] is None else self.bwd_ws[k].data_ptr(), self.stream())
         return used
 
+    def skips_bwd_exchange(self, k: int) -> bool:
+        """Layer k's backward needs no halo (ΔW¹ from the forward aggregate)."""
+        return k == 1 and self.dw1_from_fwd
+
+    def dw_from_forward(self, k: int = 1) -> int:
+        """ΔW¹ partials = (Â·H⁰)ᵀ·G¹ over all own rows; returns slots used."""
+        assert k == 1 and self.dw1_from_fwd
+        x, g = self.fwd_ws[1], self.gext[1]
+        dp, dk = self.dims[0], self.dims[1]
+        n = self.n_own
+        used = self.bwd_grids[1][2]
+        if n == 0:
+            return 0
+        with span("bwd1", 4 * n * (dp + dk) + 4 * dp * dk * used, 2 * n * dp * dk, self.stream()):
+            _lib.call("gcnb_dw_f32", x.data_ptr(), x.shape[1], dp, g.data_ptr(), g.shape[1], dk, None, n,
+                      self.partials[1].data_ptr(), self.stream())
+        return used
+
     def reduce_dw(self, k: int, n_slots: int, apply_sgd: bool = False) -> None:
         """ΔW^k = Σ of the layer's block partials (fixed order); optionally fused with SGD."""
         size = self.dw[k].numel()
@@ -523,13 +549,16 @@ class ProcState:
 
 
 def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, device=None,
-            locality: bool = False) -> list:
+            locality: bool = False, reuse_fwd_aggregate: bool = False) -> list:
     """Distribute row blocks per the partition and replicate the weights on the
     device (runtime.py:233-275).  All ranks of this process share `device`.
 
     locality=True lays each rank's own rows out by label-propagation community
     (locality.py) instead of ascending global id; `global_rows` then lists the
-    rows in that order (every host view follows it)."""
+    rows in that order (every host view follows it).
+
+    reuse_fwd_aggregate=True computes ΔW¹ from the forward's Â·H⁰ (see
+    ProcState): one aggregation and one halo exchange fewer per epoch."""
     h0 = dense(h0)
     if h0.shape != (a_hat.n_rows, model.dims[0]):
         raise ValueError(f"h0 has shape {h0.shape}, expected ({a_hat.n_rows}, {model.dims[0]})")
@@ -548,7 +577,8 @@ def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, 
     states = []
     for m in range(plan_fwd.p):
         lay = build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, m, row_labels=labels)
-        states.append(ProcState(lay, plan_fwd, plan_bwd, model, h0[lay.global_rows], dev))
+        states.append(ProcState(lay, plan_fwd, plan_bwd, model, h0[lay.global_rows], dev,
+                                reuse_fwd_aggregate=reuse_fwd_aggregate))
     return states
 
 
@@ -602,19 +632,21 @@ def _backward(states, net, n_labeled: int, epoch: int, step: int, loss_out: torc
         _lib.call("gcnb_sum_buffers_f64", _lib.ptr_array([st.loss_sum.data_ptr() for st in states]), len(states), 1,
                   loss_out.data_ptr(), states[0].stream())
     for k in range(L, 0, -1):
-        bases = _bases(states, "bwd", k)
-        for st in states:
-            st.pack_to("bwd", k, bases)
-        _log_phase(states, net, "bwd", k, epoch, step)
+        skip = states[0].skips_bwd_exchange(k)
+        if not skip:
+            bases = _bases(states, "bwd", k)
+            for st in states:
+                st.pack_to("bwd", k, bases)
+            _log_phase(states, net, "bwd", k, epoch, step)
         if len(states) == 1:
             # one rank: the ΔW reduction and the SGD step are one kernel
             st = states[0]
-            used = st.bwd_compute(k, "all")
+            used = st.dw_from_forward(k) if skip else st.bwd_compute(k, "all")
             st.reduce_dw(k, used, apply_sgd=True)
             st.dw_total[k] = st.dw[k]
             continue
         for st in states:
-            used = st.bwd_compute(k, "all")
+            used = st.dw_from_forward(k) if skip else st.bwd_compute(k, "all")
             st.reduce_dw(k, used)
         # allreduce_sum of ΔW^k in ascending rank order, then SGD on every replica.
         # Updating W^k right after its layer is exact: no later (lower) layer reads W^k.
@@ -675,7 +707,8 @@ class EpochRunner:
         for k in range(1, L + 1):
             _log_phase(self.states, net, "fwd", k, epoch, step)
         for k in range(L, 0, -1):
-            _log_phase(self.states, net, "bwd", k, epoch, step)
+            if not self.states[0].skips_bwd_exchange(k):
+                _log_phase(self.states, net, "bwd", k, epoch, step)
 
 
 def _check_scheduler(scheduler: str) -> None:

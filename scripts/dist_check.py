@@ -29,12 +29,14 @@ def main():
     ap.add_argument("--n", type=int, default=4000)
     ap.add_argument("--graph", action="store_true", help="replay captured CUDA graphs")
     ap.add_argument("--overlap", default="auto", choices=("auto", "on", "off"))
+    ap.add_argument("--wide", action="store_true", help="dims (64, 96, 40): split (workspace) layer paths")
+    ap.add_argument("--reuse", action="store_true", help="reuse_fwd_aggregate: ΔW¹ from the forward's Â·H⁰")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank)))
     torch.cuda.set_device(dev)
     dist.init_process_group(backend="gloo")
-    n, dims = args.n, (12, 16, 6)
+    n, dims = args.n, ((64, 96, 40) if args.wide else (12, 16, 6))
     raw = o.random_directed(n, 0.002, 5) if args.directed else o.random_undirected(n, 0.002, 5)
     a_hat = gb.normalize_adjacency(gb.CsrMatrix(n, n, raw.row_offsets, raw.col_indices, raw.values))
     h0 = np.random.default_rng(3).standard_normal((n, dims[0]))
@@ -43,7 +45,9 @@ def main():
     model = gb.init_model(dims, 5)
     pi = gb.random_partition(a_hat.row_nnz(), gb.PartitionConfig(p=world, seed=5, epsilon=0.05))
     tr = DistributedTrainer(a_hat, h0, pi.assignment, world, model, labels, args.directed, dev, timeout_ms=10000,
-                            overlap={"auto": None, "on": True, "off": False}[args.overlap])
+                            overlap={"auto": None, "on": True, "off": False}[args.overlap],
+                            reuse_fwd_aggregate=args.reuse)
+    assert tr.st.dw1_from_fwd == args.reuse, "reuse_fwd_aggregate needs the wide (workspace) layer-1 path"
     losses = []
     if args.graph:
         tr.capture(0, 0)
@@ -60,7 +64,7 @@ def main():
     gathered = [None] * world
     dist.all_gather_object(gathered, [w.tolist() for w in ws])
     ok = True
-    report = {"world": world, "directed": args.directed, "graph": args.graph, "losses": losses}
+    report = {"world": world, "directed": args.directed, "graph": args.graph, "reuse": args.reuse, "losses": losses}
     if rank == 0:
         w_ref, l_ref, words, _ = o.parallel_train(o.as_csr(a_hat), h0, pi.assignment, world, list(model.weights),
                                                   ids, y, args.epochs, directed=args.directed)

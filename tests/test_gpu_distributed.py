@@ -17,7 +17,9 @@ ROOT = Path(__file__).resolve().parent.parent
 
 @pytest.mark.parametrize("extra", [["--overlap", "on"], ["--directed", "--overlap", "on"],
                                    ["--directed", "--graph", "--epochs", "4", "--overlap", "on"],
-                                   ["--directed", "--graph", "--epochs", "4", "--overlap", "off"]])
+                                   ["--directed", "--graph", "--epochs", "4", "--overlap", "off"],
+                                   ["--wide", "--reuse", "--graph", "--epochs", "4", "--overlap", "on"],
+                                   ["--wide", "--reuse", "--directed", "--overlap", "off"]])
 def test_torchrun_parity(extra):
     n = torch.cuda.device_count()
     if n < 2:

@@ -277,3 +277,29 @@ def test_wide_layers_split_paths_against_oracle(directed):
     assert [m.total_words for m in metrics] == words
     for w, wr in zip(states[1].weights, w_ref):
         close(w, wr)
+
+
+@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("directed", [False, True])
+def test_reuse_fwd_aggregate_against_oracle(directed, p):
+    """ΔW¹ = (Â·H⁰)ᵀ·G¹ from the forward's aggregate (reuse_fwd_aggregate):
+    losses and weights match the oracle within TOL, and the message log drops
+    exactly the layer-1 backward exchange (reference words minus rows × d_1)."""
+    n, dims = 3000, (64, 96, 40)
+    raw = o.random_directed(n, 0.003, 6) if directed else o.random_undirected(n, 0.003, 6)
+    a_hat = gb.normalize_adjacency(gb.CsrMatrix(n, n, raw.row_offsets, raw.col_indices, raw.values))
+    h0 = np.random.default_rng(7).standard_normal((n, dims[0]))
+    ids, y = o.random_labels(n, dims[-1], 300, 6)
+    model = gb.init_model(dims, 6)
+    pi = gb.random_partition(a_hat.row_nnz(), gb.PartitionConfig(p=p, seed=6, epsilon=0.1))
+    states = gb.scatter(a_hat, h0, pi, model, directed=directed, locality=True, reuse_fwd_aggregate=True)
+    assert all(st.dw1_from_fwd for st in states)
+    metrics = gb.train_epochs(states, gb.DeviceNetwork(p), gb.LabelSet(ids, y, dims[-1]), 3)
+    w_ref, losses, words, _ = o.parallel_train(o.as_csr(a_hat), h0, pi.assignment, p, list(model.weights), ids, y,
+                                               3, directed=directed)
+    close([m.loss for m in metrics], losses)
+    for w, wr in zip(states[-1].weights, w_ref):
+        close(w, wr)
+    plan_b = states[0].plan_bwd
+    bwd_rows = sum(len(plan_b.send[m][q]) for m in range(p) for q in range(p) if m != q)
+    assert [m.total_words for m in metrics] == [w - bwd_rows * dims[1] for w in words]
