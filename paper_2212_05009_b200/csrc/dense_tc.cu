@@ -23,7 +23,6 @@ namespace gcnb {
 
 namespace {
 
-constexpr int TC_THREADS = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -474,8 +473,18 @@ int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_
 // with plain 16-byte cp.async.  The accumulator lives in TMEM for the CTA's
 // whole tile range and is written once; partials fold in fixed order
 // (k_reduce*), so results are deterministic.
-//   ΔW += H·A + lo(H)·A  [lo(H) in its own buffer],  then A → lo(A) in place,  ΔW += H·lo(A)
-constexpr int DW_T = 64;  // rows per tile (8 MMA K-steps of 8 rows)
+//   ΔW += H·A + lo(H)·A + H·lo(A)
+// Warp-specialised pipeline over DW_T-row tiles and S stages (raw H, raw A,
+// lo(H), lo(A) per stage):
+//   warps 0-3  converter (lo buffers of each landed stage), then the final
+//              TMEM → partial epilogue
+//   warps 4-7  producer (cp.async rows, zero-filled past the end)
+//   warp 8     TMEM owner; lane 0 issues the 3 × DW_T/8 MMAs of a tile
+constexpr int DW_T = 32;            // rows per tile (4 MMA K-steps of 8 rows)
+constexpr int DW_WARPS = 9;
+constexpr int DW_THREADS = DW_WARPS * 32;
+constexpr int DW_MAX_STAGES = 4;
+constexpr int DW_NA_H = 4;          // M = 128 features = 4 atoms
 
 namespace {
 
@@ -486,8 +495,9 @@ __device__ __forceinline__ uint32_t mn_off(int k, int m, int na) {
 }
 
 __device__ __forceinline__ void load_rows_mn(uint32_t stage, const float* __restrict__ X, int ldx,
-                                             const int* __restrict__ rows, int n_rows, int m0, int kc, int na) {
-  for (int idx = threadIdx.x; idx < DW_T * kc; idx += TC_THREADS) {
+                                             const int* __restrict__ rows, int n_rows, int m0, int kc, int na,
+                                             int tid) {
+  for (int idx = tid; idx < DW_T * kc; idx += 128) {
     const int k = idx / kc, c = idx - k * kc;
     const int i = m0 + k;
     const bool ok = i < n_rows;  // rows past the end must be zero: they are summed over
@@ -496,7 +506,6 @@ __device__ __forceinline__ void load_rows_mn(uint32_t stage, const float* __rest
                  "l"(X + (size_t)xr * ldx + 4 * c), "r"(ok ? 16 : 0)
                  : "memory");
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 __device__ __forceinline__ uint64_t desc_mn_sw32(uint32_t addr, int na) {
@@ -504,113 +513,144 @@ __device__ __forceinline__ uint64_t desc_mn_sw32(uint32_t addr, int na) {
   return smem_desc(addr, 512, (uint32_t)na * 512) | (1ull << 61);
 }
 
-__device__ __forceinline__ void lo_inplace(uint8_t* dst, const uint8_t* src, int bytes) {
-  for (int i = threadIdx.x; i < bytes / 16; i += TC_THREADS) {
+__device__ __forceinline__ void lo_copy(uint8_t* dst, const uint8_t* src, int bytes, int tid) {
+  for (int i = tid; i < bytes / 16; i += 128) {
     const float4 v = reinterpret_cast<const float4*>(src)[i];
     reinterpret_cast<float4*>(dst)[i] = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
   }
 }
 
+struct DwGeom {
+  int na_a, h_bytes, a_bytes, st_bytes, stages;
+};
+
+__host__ __device__ inline DwGeom dw_geom(int d_k) {
+  DwGeom g;
+  const int Np = (d_k + 15) & ~15;
+  g.na_a = (Np + 31) / 32;
+  g.h_bytes = (DW_T / 4) * DW_NA_H * 512;
+  g.a_bytes = (DW_T / 4) * g.na_a * 512;
+  g.st_bytes = 2 * (g.h_bytes + g.a_bytes);
+  const int fit = (int)((size_t)(220 * 1024) / (size_t)g.st_bytes);
+  g.stages = fit < DW_MAX_STAGES ? fit : DW_MAX_STAGES;
+  return g;
+}
+
 }  // namespace
 
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(DW_THREADS, 1)
     k_dw_tc(const float* __restrict__ H, int ldh, int d_prev, const float* __restrict__ A, int lda, int d_k,
             const int* __restrict__ rows, int n_rows, float* __restrict__ partials, int n_slots) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t bars[3 * DW_MAX_STAGES + 1];
   __shared__ uint32_t tmem_base_slot;
-  constexpr int NA_H = 4;                                // M = 128 features = 4 atoms
-  const int Np = (d_k + 15) & ~15, na_a = (Np + 31) / 32;
+  const DwGeom g = dw_geom(d_k);
+  const int S = g.stages;
+  const int Np = (d_k + 15) & ~15;
   const int kc_h = (d_prev + 3) / 4, kc_a = (d_k + 3) / 4;
-  const int h_bytes = (DW_T / 4) * NA_H * 512, a_bytes = (DW_T / 4) * na_a * 512;
-  uint8_t* st_h[2] = {smem, smem + h_bytes + a_bytes};
-  uint8_t* st_a[2] = {smem + h_bytes, smem + 2 * h_bytes + a_bytes};
-  uint8_t* h_lo = smem + 2 * (h_bytes + a_bytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (n_rows + DW_T - 1) / DW_T;
   const uint32_t tmem_cols = Np <= 32 ? 32 : Np <= 64 ? 64 : Np <= 128 ? 128 : 256;
+  // stage s: [H | A | lo(H) | lo(A)]
+  auto st_h = [&](int s) { return smem + s * g.st_bytes; };
+  auto st_a = [&](int s) { return smem + s * g.st_bytes + g.h_bytes; };
+  auto st_hl = [&](int s) { return smem + s * g.st_bytes + g.h_bytes + g.a_bytes; };
+  auto st_al = [&](int s) { return smem + s * g.st_bytes + 2 * g.h_bytes + g.a_bytes; };
+  // barriers: full[S] (producers) conv[S] (converters) empty[S] (MMA commit) | done
+  auto bar = [&](int kind, int i) { return smem_u32(&bars[kind * DW_MAX_STAGES + i]); };
+  const uint32_t b_done = smem_u32(&bars[3 * DW_MAX_STAGES]);
+  if (smem_u32(smem) & 1023u) __trap();
 
-  // pad features (never loaded) must read as zero: clear everything once
-  for (int i = threadIdx.x; i < (3 * h_bytes + 2 * a_bytes) / 16; i += TC_THREADS)
+  // pad features (never loaded) must read as zero in every buffer: clear once
+  for (int i = threadIdx.x; i < S * g.st_bytes / 16; i += DW_THREADS)
     reinterpret_cast<float4*>(smem)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncthreads();
-  if ((int)blockIdx.x < n_tiles) {
-    load_rows_mn(smem_u32(st_h[0]), H, ldh, rows, n_rows, blockIdx.x * DW_T, kc_h, NA_H);
-    load_rows_mn(smem_u32(st_a[0]), A, lda, rows, n_rows, blockIdx.x * DW_T, kc_a, na_a);
-  }
-  if (warp == 0) {
+  if (warp == 8) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_slot)),
                  "r"(tmem_cols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)) : "memory");
+    for (int i = 0; i < S; ++i) {
+      mbar_init(bar(0, i), 128);
+      mbar_init(bar(1, i), 128);
+      mbar_init(bar(2, i), 1);
+    }
+    mbar_init(b_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  fence_async_smem();
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
   const uint32_t tmem = tmem_base_slot;
-  const uint32_t mb = smem_u32(&mbar);
-  const uint32_t idesc = idesc_tf32(128, Np) | (1u << 15) | (1u << 16);  // A and B MN-major
-  const uint32_t kstep_h = 2 * NA_H * 512, kstep_a = 2 * na_a * 512;   // 8 rows = two 4-row groups
-  uint32_t phase = 0;
-  bool first = true;
 
-  int it = 0;
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
-    const int next = tile + gridDim.x;
-    if (next < n_tiles) {
-      load_rows_mn(smem_u32(st_h[(it + 1) & 1]), H, ldh, rows, n_rows, next * DW_T, kc_h, NA_H);
-      load_rows_mn(smem_u32(st_a[(it + 1) & 1]), A, lda, rows, n_rows, next * DW_T, kc_a, na_a);
-      asm volatile("cp.async.wait_group 2;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    uint8_t* hs = st_h[it & 1];
-    uint8_t* as = st_a[it & 1];
-    lo_inplace(h_lo, hs, h_bytes);
-    fence_async_smem();
-    __syncthreads();
-    const uint32_t ha = smem_u32(hs), hl = smem_u32(h_lo), aa = smem_u32(as);
-    if (threadIdx.x == 0) {
-      tc_after_sync();
-      for (int s = 0; s < DW_T / 8; ++s) {
-        const uint64_t db = desc_mn_sw32(aa + s * kstep_a, na_a);
-        mma_tf32(tmem, desc_mn_sw32(ha + s * kstep_h, NA_H), db, idesc, first ? 0u : 1u);
-        first = false;
-        mma_tf32(tmem, desc_mn_sw32(hl + s * kstep_h, NA_H), db, idesc, 1u);
+  if (warp >= 4 && warp < 8) {
+    // ---------------- producer
+    const int tid = threadIdx.x - 128;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+      const int s = t % S;
+      if (t >= S) mbar_wait(bar(2, s), (uint32_t)(t / S - 1) & 1u);
+      load_rows_mn(smem_u32(st_h(s)), H, ldh, rows, n_rows, tile * DW_T, kc_h, DW_NA_H, tid);
+      load_rows_mn(smem_u32(st_a(s)), A, lda, rows, n_rows, tile * DW_T, kc_a, g.na_a, tid);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (t >= 1) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        fence_async_smem();
+        mbar_arrive(bar(0, (t - 1) % S));
       }
-      mma_commit(mb);
     }
-    mbar_wait(mb, phase);
-    phase ^= 1;
-    lo_inplace(as, as, a_bytes);
-    fence_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tc_after_sync();
-      for (int s = 0; s < DW_T / 8; ++s)
-        mma_tf32(tmem, desc_mn_sw32(ha + s * kstep_h, NA_H), desc_mn_sw32(aa + s * kstep_a, na_a), idesc, 1u);
-      mma_commit(mb);
+    if (t >= 1) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      fence_async_smem();
+      mbar_arrive(bar(0, (t - 1) % S));
     }
-    mbar_wait(mb, phase);
-    phase ^= 1;
-    __syncthreads();  // stage (it & 1) and lo(H) free for reuse
-  }
-  tc_after_sync();
-  // partial[m][n] for m < d_prev, n < round4(d_k): TMEM lane m, column n
-  const int ld_k = (d_k + 3) & ~3;
-  {
-    const int quarter = warp & 3, half = warp >> 2;
-    const int m = quarter * 32 + lane;
+  } else if (warp == 8) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_tf32(128, Np) | (1u << 15) | (1u << 16);  // A and B MN-major
+      const uint32_t kstep_h = 2 * DW_NA_H * 512, kstep_a = 2 * g.na_a * 512;  // 8 rows = two 4-row groups
+      int t = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+        const int s = t % S;
+        mbar_wait(bar(1, s), (uint32_t)(t / S) & 1u);
+        tc_after_sync();
+        const uint32_t ha = smem_u32(st_h(s)), hl = smem_u32(st_hl(s));
+        const uint32_t aa = smem_u32(st_a(s)), al = smem_u32(st_al(s));
+        for (int k = 0; k < DW_T / 8; ++k) {
+          const uint64_t dh = desc_mn_sw32(ha + k * kstep_h, DW_NA_H);
+          const uint64_t da = desc_mn_sw32(aa + k * kstep_a, g.na_a);
+          mma_tf32(tmem, dh, da, idesc, (t > 0 || k > 0) ? 1u : 0u);
+          mma_tf32(tmem, desc_mn_sw32(hl + k * kstep_h, DW_NA_H), da, idesc, 1u);
+          mma_tf32(tmem, dh, desc_mn_sw32(al + k * kstep_a, g.na_a), idesc, 1u);
+        }
+        mma_commit(bar(2, s));
+      }
+      mma_commit(b_done);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- converter (warps 0-3), then the epilogue
+    const int tid = threadIdx.x;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+      const int s = t % S;
+      mbar_wait(bar(0, s), (uint32_t)(t / S) & 1u);
+      lo_copy(st_hl(s), st_h(s), g.h_bytes, tid);
+      lo_copy(st_al(s), st_a(s), g.a_bytes, tid);
+      fence_async_smem();
+      mbar_arrive(bar(1, s));
+    }
+    if (n_tiles > (int)blockIdx.x) mbar_wait(b_done, 0);
+    tc_after_sync();
+    // partial[m][n] for m < d_prev, n < round4(d_k): TMEM lane m, column n
+    const int ld_k = (d_k + 3) & ~3;
+    const int m = warp * 32 + lane;
     float* out = partials + (size_t)blockIdx.x * d_prev * ld_k + (size_t)m * ld_k;
-    const int c_lo = half * (Np / 2), c_hi = c_lo + Np / 2;
-    for (int c0 = c_lo; c0 < c_hi; c0 += 8) {
+    for (int c0 = 0; c0 < Np; c0 += 8) {
       uint32_t v[8];
-      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
           : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
@@ -625,20 +665,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   // slots beyond the grid (the caller sized the partials for another engine) are zero
   {
+    const int ld_k = (d_k + 3) & ~3;
     const size_t slot = (size_t)d_prev * ld_k;
     for (int sl = blockIdx.x + gridDim.x; sl < n_slots; sl += gridDim.x)
-      for (size_t e = threadIdx.x; e < slot; e += TC_THREADS) partials[sl * slot + e] = 0.0f;
+      for (size_t e = threadIdx.x; e < slot; e += DW_THREADS) partials[sl * slot + e] = 0.0f;
   }
   tc_before_sync();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
+  tc_after_sync();
+  if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
 }
 
 bool dw_tc_applies(int d_prev, int d_k) {
   if (g_dense_mode == 1) return false;
-  const int Np = (d_k + 15) & ~15, na = (Np + 31) / 32;
-  const size_t smem = (size_t)3 * (DW_T / 4) * 4 * 512 + (size_t)2 * (DW_T / 4) * na * 512;
-  return d_prev <= 128 && d_k <= 256 && smem <= 220 * 1024;
+  return d_prev <= 128 && d_k <= 256 && dw_geom(d_k).stages >= 2;
 }
 
 int dw_tc_grid(int n_rows) { return std::max(1, std::min((n_rows + DW_T - 1) / DW_T, num_sms())); }
@@ -646,10 +686,10 @@ int dw_tc_grid(int n_rows) { return std::max(1, std::min((n_rows + DW_T - 1) / D
 int launch_dw_tc(const float* h, int ldh, int d_prev, const float* a, int lda, int d_k, const int* rows, int n_rows,
                  float* partials, int n_slots, cudaStream_t st) {
   const int grid = std::min(dw_tc_grid(n_rows), n_slots);
-  const int Np = (d_k + 15) & ~15, na = (Np + 31) / 32;
-  const size_t smem = (size_t)3 * (DW_T / 4) * 4 * 512 + (size_t)2 * (DW_T / 4) * na * 512;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_dw_tc<<<grid, TC_THREADS, smem, st>>>(h, ldh, d_prev, a, lda, d_k, rows, n_rows, partials, n_slots);
+  const DwGeom g = dw_geom(d_k);
+  const size_t smem = (size_t)g.stages * g.st_bytes;
+  cudaFuncSetAttribute(k_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_dw_tc<<<grid, DW_THREADS, smem, st>>>(h, ldh, d_prev, a, lda, d_k, rows, n_rows, partials, n_slots);
   GCNB_AFTER_LAUNCH("bwd ΔW (tcgen05 3xTF32)");
   return GCNB_OK;
 }
