@@ -13,8 +13,11 @@
 // k_dense_tc: Y[r] = act(X[r]·W) or (X[r]·Wᵀ) ⊙ σ'(H[r]) — warp-specialised,
 // persistent, MMA M = output features (see the kernel comment).
 // k_dw_tc:    per-CTA ΔW partials Σ_r H[r]ᵀ·A[r] with K = graph rows.
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <cstdio>
 
 #include "common.cuh"
@@ -160,6 +163,19 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+
+// TMA: box at (x, y) of a 2-D tensor map into shared memory, completion counted on mbar
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(mbar)
+      : "memory");
+}
+
 // X rows [m0, m0+N) (through the row list) into a K-major SWIZZLE_128B tile.
 __device__ __forceinline__ void load_x_rows(uint32_t stage, const float* __restrict__ X, int ldx,
                                             const int* __restrict__ rows, int n_rows, int m0, int N, int kc, int tid) {
@@ -188,11 +204,16 @@ __device__ __forceinline__ void load_mask_rows(uint32_t stage, const float* __re
 
 }  // namespace
 
-template <bool RELU, bool MASKED>
+// TMA (rows == nullptr): one thread of warp 8 streams each tile with Kb/32
+// SWIZZLE_128B boxes of 32 floats × NT_ rows (out-of-range K and rows arrive
+// as zeros) plus, masked, one box of the mask rows; completion is counted by
+// the stage's mbarrier (expect_tx), so loads run up to S tiles ahead.
+template <bool RELU, bool MASKED, bool TMA>
 __global__ void __launch_bounds__(DT_THREADS, 1)
     k_dense_tc(const float* __restrict__ X, int ldx, const int* __restrict__ rows, int n_rows, int K,
                const float* __restrict__ W, int ldw, int w_nk, int M, int NT_, int S, float* __restrict__ Y,
-               int ldy, const float* __restrict__ Hm, int ldhm) {
+               int ldy, const float* __restrict__ Hm, int ldhm, const __grid_constant__ CUtensorMap tmx,
+               const __grid_constant__ CUtensorMap tmm) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[4 * DT_MAX_STAGES + 4];
   __shared__ uint32_t tmem_base_slot;
@@ -224,7 +245,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(bar(0, i), DT_PROD);
+      mbar_init(bar(0, i), TMA ? 1 : DT_PROD);
       mbar_init(bar(1, i), 1);
       mbar_init(bar(2, i), DT_CONV);
       mbar_init(bar(3, i), MASKED ? 1 + DT_EPI : 1);
@@ -269,8 +290,23 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
   __syncthreads();
   tc_after_sync();
 
-  if (warp >= 8 && warp < 12) {
-    // ---------------- producer
+  if (TMA && warp >= 8 && warp < 12) {
+    // ---------------- producer (TMA)
+    if (warp == 8 && lane == 0) {
+      const uint32_t tx = (uint32_t)(Kb / 32) * NT_ * 128 + (MASKED ? (uint32_t)NT_ * mpad * 4 : 0u);
+      int t = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+        const int s = t % S;
+        if (t >= S) mbar_wait(bar(3, s), (uint32_t)(t / S - 1) & 1u);
+        const uint32_t st = smem_u32(smem + s * st_bytes);
+        mbar_expect_tx(bar(0, s), tx);
+        for (int j = 0; j < Kb / 32; ++j) tma_load_2d(st + j * NT_ * 128, &tmx, 32 * j, tile * NT_, bar(0, s));
+        if (MASKED) tma_load_2d(st + x_bytes, &tmm, 0, tile * NT_, bar(0, s));
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 8 && warp < 12) {
+    // ---------------- producer (cp.async, row list)
     const int tid = threadIdx.x - 256;
     int t = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
@@ -409,18 +445,18 @@ namespace {
 constexpr size_t DT_SMEM_MAX = 227 * 1024 - 1024;
 
 // Rows per tile (MMA N) and stage count: the largest tile of 128/64/32 rows
-// for which at least three stages fit (up to DT_MAX_STAGES).  Three is the
-// minimum: the producer signals tile t-1 only after it has waited for the
-// stage of tile t to drain (lo MMAs of tile t-S), while the MMA issuer needs
-// tile t-1 before it issues those lo MMAs of tile t-2 — with S = 2 that is a
-// cycle.
-int dense_tc_tile(int d_in, int d_out, bool masked, int* stages, size_t* smem_out) {
+// for which enough stages fit (up to DT_MAX_STAGES).  The cp.async producer
+// needs three: it signals tile t-1 only after it has waited for the stage of
+// tile t to drain (lo MMAs of tile t-S), while the MMA issuer needs tile t-1
+// before it issues those lo MMAs of tile t-2 — with S = 2 that is a cycle.
+// TMA completion does not wait on later tiles, so two suffice there.
+int dense_tc_tile(int d_in, int d_out, bool masked, bool tma, int* stages, size_t* smem_out) {
   if (d_in > 128 || d_out > 128) return 0;  // Wᵀ hi+lo ≤ 256 TMEM columns; one 128-lane half
   const int Kb = (d_in + 31) & ~31, mpad = (d_out + 3) & ~3;
   for (int nt = 128; nt >= 32; nt >>= 1) {
     const size_t st = ((size_t)nt * (Kb + (masked ? mpad : 0)) * 4 + 1023) & ~(size_t)1023;
     const int s = (int)std::min<size_t>(DT_MAX_STAGES, DT_SMEM_MAX / st);
-    if (s >= 3) {
+    if (s >= (tma ? 2 : 3)) {
       *stages = s;
       *smem_out = s * st;
       return nt;
@@ -435,28 +471,80 @@ bool dense_tc_applies(int d_in, int d_out) {
   int stages = 0;
   size_t smem = 0;
   // the backward form carries a mask tile: require that it fits too
-  const bool fits = dense_tc_tile(d_in, d_out, true, &stages, &smem) > 0;
+  const bool fits = dense_tc_tile(d_in, d_out, true, false, &stages, &smem) > 0;
   if (g_dense_mode == 2) return fits;
   return fits && d_in >= 32 && d_out >= 32;
 }
 
+namespace {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D fp32 tensor map: dim0 = `cols` contiguous floats, dim1 = `n_rows` rows
+// `ld` floats apart; box {box0, box1}; out-of-range elements read as zero.
+bool tmap_2d(CUtensorMap* m, const float* base, int cols, int n_rows, int ld, int box0, int box1,
+             CUtensorMapSwizzle sw) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)n_rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)box1};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
 int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
                     float* y, int ldy, int act, cudaStream_t st, const float* w_nk, int ld_wnk, const float* hmask,
                     int ldhm) {
+  const bool masked = hmask != nullptr;
+  const int mpad = (d_out + 3) & ~3;
+  CUtensorMap tmx, tmm;
+  std::memset(&tmx, 0, sizeof(tmx));
+  std::memset(&tmm, 0, sizeof(tmm));
   int stages = 0;
   size_t smem = 0;
-  const int nt = dense_tc_tile(d_in, d_out, hmask != nullptr, &stages, &smem);
+  bool tma = rows == nullptr && n_rows > 0;
+  int nt = tma ? dense_tc_tile(d_in, d_out, masked, true, &stages, &smem) : 0;
+  if (tma) {
+    tma = nt > 0 && tmap_2d(&tmx, x, d_in, n_rows, ldx, 32, nt, CU_TENSOR_MAP_SWIZZLE_128B) &&
+          (!masked || tmap_2d(&tmm, hmask, mpad, n_rows, ldhm, mpad, nt, CU_TENSOR_MAP_SWIZZLE_NONE));
+  }
+  if (!tma) nt = dense_tc_tile(d_in, d_out, masked, false, &stages, &smem);
   GCNB_REQUIRE(nt > 0, "dense (tcgen05): widths %d -> %d not supported", d_in, d_out);
-  GCNB_REQUIRE(!hmask || ldhm >= ((d_out + 3) & ~3), "dense (tcgen05): mask stride too small");
+  GCNB_REQUIRE(!hmask || ldhm >= mpad, "dense (tcgen05): mask stride too small");
   const bool relu = act == GCNB_ACT_RELU;
-  auto fn = hmask ? (relu ? k_dense_tc<true, true> : k_dense_tc<false, true>)
-                  : (relu ? k_dense_tc<true, false> : k_dense_tc<false, false>);
+  using Fn = void (*)(const float*, int, const int*, int, int, const float*, int, int, int, int, int, float*, int,
+                      const float*, int, const CUtensorMap, const CUtensorMap);
+  Fn fn;
+  if (tma) fn = masked ? (relu ? k_dense_tc<true, true, true> : k_dense_tc<false, true, true>)
+                       : (relu ? k_dense_tc<true, false, true> : k_dense_tc<false, false, true>);
+  else fn = masked ? (relu ? k_dense_tc<true, true, false> : k_dense_tc<false, true, false>)
+                   : (relu ? k_dense_tc<true, false, false> : k_dense_tc<false, false, false>);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles = (n_rows + nt - 1) / nt;
   const int grid = std::max(1, std::min(tiles, num_sms()));
   fn<<<grid, DT_THREADS, smem, st>>>(x, ldx, rows, n_rows, d_in, w_nk ? w_nk : w, w_nk ? ld_wnk : round4(d_out),
-                                     w_nk ? 1 : 0, d_out, nt, stages, y, ldy, hmask, ldhm);
-  GCNB_AFTER_LAUNCH("dense (tcgen05 3xTF32)");
+                                     w_nk ? 1 : 0, d_out, nt, stages, y, ldy, hmask, ldhm, tmx, tmm);
+  GCNB_AFTER_LAUNCH(tma ? "dense (tcgen05 3xTF32, TMA)" : "dense (tcgen05 3xTF32)");
   return GCNB_OK;
 }
 
