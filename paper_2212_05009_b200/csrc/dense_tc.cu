@@ -576,29 +576,30 @@ constexpr int DW_NA_H = 4;          // M = 128 features = 4 atoms
 
 namespace {
 
-// Byte offset of feature m of tile row k in an MN-major SW128_32B tile with `na` atoms per 4-row group.
-__device__ __forceinline__ uint32_t mn_off(int k, int m, int na) {
-  return (uint32_t)((k >> 2) * (na * 512) + (m >> 5) * 512 + (k & 3) * 128 + ((((m & 31) >> 3) ^ (k & 3)) << 5) +
-                    ((m & 7) << 2));
+// Byte offset of feature m of tile row k in an MN-major SW128_32B tile: each
+// 32-feature atom holds the tile's DW_T rows contiguously (128 bytes per row,
+// its 32-byte granules XOR-permuted by k & 3) — the layout a TMA box of
+// {32 features, DW_T rows} with SWIZZLE_128B_ATOM_32B writes.
+__device__ __forceinline__ uint32_t mn_off(int k, int m) {
+  return (uint32_t)((m >> 5) * (DW_T * 128) + k * 128 + ((((m & 31) >> 3) ^ (k & 3)) << 5) + ((m & 7) << 2));
 }
 
 __device__ __forceinline__ void load_rows_mn(uint32_t stage, const float* __restrict__ X, int ldx,
-                                             const int* __restrict__ rows, int n_rows, int m0, int kc, int na,
-                                             int tid) {
+                                             const int* __restrict__ rows, int n_rows, int m0, int kc, int tid) {
   for (int idx = tid; idx < DW_T * kc; idx += 128) {
     const int k = idx / kc, c = idx - k * kc;
     const int i = m0 + k;
     const bool ok = i < n_rows;  // rows past the end must be zero: they are summed over
     const int xr = ok ? (rows ? __ldg(rows + i) : i) : 0;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(stage + mn_off(k, 4 * c, na)),
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(stage + mn_off(k, 4 * c)),
                  "l"(X + (size_t)xr * ldx + 4 * c), "r"(ok ? 16 : 0)
                  : "memory");
   }
 }
 
-__device__ __forceinline__ uint64_t desc_mn_sw32(uint32_t addr, int na) {
-  // LBO = next 32-feature atom (512 B), SBO = next 4-row group, layout type 1
-  return smem_desc(addr, 512, (uint32_t)na * 512) | (1ull << 61);
+__device__ __forceinline__ uint64_t desc_mn_sw32(uint32_t addr) {
+  // LBO = next 32-feature atom (DW_T rows × 128 B), SBO = next 4-row group (512 B), layout type 1
+  return smem_desc(addr, DW_T * 128, 512) | (1ull << 61);
 }
 
 __device__ __forceinline__ void lo_copy(uint8_t* dst, const uint8_t* src, int bytes, int tid) {
@@ -626,9 +627,11 @@ __host__ __device__ inline DwGeom dw_geom(int d_k) {
 
 }  // namespace
 
+template <bool TMA>
 __global__ void __launch_bounds__(DW_THREADS, 1)
     k_dw_tc(const float* __restrict__ H, int ldh, int d_prev, const float* __restrict__ A, int lda, int d_k,
-            const int* __restrict__ rows, int n_rows, float* __restrict__ partials, int n_slots) {
+            const int* __restrict__ rows, int n_rows, float* __restrict__ partials, int n_slots,
+            const __grid_constant__ CUtensorMap tmh, const __grid_constant__ CUtensorMap tma_) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[3 * DW_MAX_STAGES + 1];
   __shared__ uint32_t tmem_base_slot;
@@ -660,7 +663,7 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(bar(0, i), 128);
+      mbar_init(bar(0, i), TMA ? 1 : 128);
       mbar_init(bar(1, i), 128);
       mbar_init(bar(2, i), 1);
     }
@@ -673,15 +676,31 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
   tc_after_sync();
   const uint32_t tmem = tmem_base_slot;
 
-  if (warp >= 4 && warp < 8) {
-    // ---------------- producer
+  if (TMA && warp >= 4 && warp < 8) {
+    // ---------------- producer (TMA: one box per 32-feature atom of H and A)
+    if (warp == 4 && lane == 0) {
+      const uint32_t tx = (uint32_t)(DW_NA_H + g.na_a) * DW_T * 128;
+      int t = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+        const int s = t % S;
+        if (t >= S) mbar_wait(bar(2, s), (uint32_t)(t / S - 1) & 1u);
+        mbar_expect_tx(bar(0, s), tx);
+        for (int a = 0; a < DW_NA_H; ++a)
+          tma_load_2d(smem_u32(st_h(s)) + a * DW_T * 128, &tmh, 32 * a, tile * DW_T, bar(0, s));
+        for (int a = 0; a < g.na_a; ++a)
+          tma_load_2d(smem_u32(st_a(s)) + a * DW_T * 128, &tma_, 32 * a, tile * DW_T, bar(0, s));
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- producer (cp.async, row list)
     const int tid = threadIdx.x - 128;
     int t = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
       const int s = t % S;
       if (t >= S) mbar_wait(bar(2, s), (uint32_t)(t / S - 1) & 1u);
-      load_rows_mn(smem_u32(st_h(s)), H, ldh, rows, n_rows, tile * DW_T, kc_h, DW_NA_H, tid);
-      load_rows_mn(smem_u32(st_a(s)), A, lda, rows, n_rows, tile * DW_T, kc_a, g.na_a, tid);
+      load_rows_mn(smem_u32(st_h(s)), H, ldh, rows, n_rows, tile * DW_T, kc_h, tid);
+      load_rows_mn(smem_u32(st_a(s)), A, lda, rows, n_rows, tile * DW_T, kc_a, tid);
       asm volatile("cp.async.commit_group;" ::: "memory");
       if (t >= 1) {
         asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -698,7 +717,7 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
     // ---------------- MMA issuer
     if (lane == 0) {
       const uint32_t idesc = idesc_tf32(128, Np) | (1u << 15) | (1u << 16);  // A and B MN-major
-      const uint32_t kstep_h = 2 * DW_NA_H * 512, kstep_a = 2 * g.na_a * 512;  // 8 rows = two 4-row groups
+      const uint32_t kstep = 2 * 512;  // 8 rows = two 4-row groups
       int t = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
         const int s = t % S;
@@ -707,11 +726,11 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
         const uint32_t ha = smem_u32(st_h(s)), hl = smem_u32(st_hl(s));
         const uint32_t aa = smem_u32(st_a(s)), al = smem_u32(st_al(s));
         for (int k = 0; k < DW_T / 8; ++k) {
-          const uint64_t dh = desc_mn_sw32(ha + k * kstep_h, DW_NA_H);
-          const uint64_t da = desc_mn_sw32(aa + k * kstep_a, g.na_a);
+          const uint64_t dh = desc_mn_sw32(ha + k * kstep);
+          const uint64_t da = desc_mn_sw32(aa + k * kstep);
           mma_tf32(tmem, dh, da, idesc, (t > 0 || k > 0) ? 1u : 0u);
-          mma_tf32(tmem, desc_mn_sw32(hl + k * kstep_h, DW_NA_H), da, idesc, 1u);
-          mma_tf32(tmem, dh, desc_mn_sw32(al + k * kstep_a, g.na_a), idesc, 1u);
+          mma_tf32(tmem, desc_mn_sw32(hl + k * kstep), da, idesc, 1u);
+          mma_tf32(tmem, dh, desc_mn_sw32(al + k * kstep), idesc, 1u);
         }
         mma_commit(bar(2, s));
       }
@@ -776,9 +795,16 @@ int launch_dw_tc(const float* h, int ldh, int d_prev, const float* a, int lda, i
   const int grid = std::min(dw_tc_grid(n_rows), n_slots);
   const DwGeom g = dw_geom(d_k);
   const size_t smem = (size_t)g.stages * g.st_bytes;
-  cudaFuncSetAttribute(k_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_dw_tc<<<grid, DW_THREADS, smem, st>>>(h, ldh, d_prev, a, lda, d_k, rows, n_rows, partials, n_slots);
-  GCNB_AFTER_LAUNCH("bwd ΔW (tcgen05 3xTF32)");
+  CUtensorMap tmh, tma_;
+  std::memset(&tmh, 0, sizeof(tmh));
+  std::memset(&tma_, 0, sizeof(tma_));
+  const bool tma = rows == nullptr && n_rows > 0 &&
+                   tmap_2d(&tmh, h, d_prev, n_rows, ldh, 32, DW_T, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
+                   tmap_2d(&tma_, a, d_k, n_rows, lda, 32, DW_T, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  auto fn = tma ? k_dw_tc<true> : k_dw_tc<false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  fn<<<grid, DW_THREADS, smem, st>>>(h, ldh, d_prev, a, lda, d_k, rows, n_rows, partials, n_slots, tmh, tma_);
+  GCNB_AFTER_LAUNCH(tma ? "bwd ΔW (tcgen05 3xTF32, TMA)" : "bwd ΔW (tcgen05 3xTF32)");
   return GCNB_OK;
 }
 
