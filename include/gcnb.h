@@ -133,6 +133,9 @@ int gcnb_dense_f32(const float* x, int32_t ldx, const int32_t* rows, int32_t n_r
  * everywhere, 2 = tcgen05 wherever the tile fits shared memory.  Both engines
  * meet the 1e-4 fp32 bar; they differ in the last bits. */
 int gcnb_set_dense_mode(int32_t mode);
+/* Test/tuning knob: force the (lanes per row, float4 chunks per lane) shape of
+ * the aggregation kernel for every width it covers (0, 0 = automatic). */
+int gcnb_set_agg_shape(int32_t lpr, int32_t vpl);
 
 /* runtime._bwd_compute (runtime.py:344-356) for the row list `rows`:
  *   agg[r]   = A_back[r,:]·G                       (G extended, d_k wide)

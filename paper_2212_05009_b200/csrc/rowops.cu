@@ -183,6 +183,11 @@ __device__ __forceinline__ void aggregate_row(const int* __restrict__ rp, const 
 }
 
 // ---------------------------------------------------------------------------
+// Gathers batched per lane before one cp.async wait: ~8 float4 chunks in flight.
+__host__ __device__ constexpr int agg_batch(int lpr, int vpl) {
+  return lpr < 8 / vpl ? lpr : (8 / vpl > 0 ? 8 / vpl : 1);
+}
+
 // Aggregate-only: Y[r] = act(A[r,:]·X)  (act < 0: plain store)
 //
 // Rows are handed out dynamically: a warp grabs the next AGG_ROWS_PER_GRAB
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
   const int lane = threadIdx.x & 31;
   const int gl = lane & (LPR - 1);
   const int gw = lane / LPR;
-  constexpr int U = LPR < 8 ? LPR : 8;
+  constexpr int U = agg_batch(LPR, VPL);
   extern __shared__ __align__(16) float4 stage_all[];
   float4* stage = stage_all + (threadIdx.x >> 5) * (U * VPL * 32);
   auto grab = [&]() {
@@ -604,6 +609,9 @@ struct AggShape {
   int vpl;
 };
 
+// Forced (lpr, vpl) for the aggregation-only kernel (gcnb_set_agg_shape; 0 = auto).
+int g_agg_lpr = 0, g_agg_vpl = 0;
+
 AggShape agg_shape(int d) {
   const int c4 = round4(d) / 4;
   if (c4 > 32) return {32, (c4 + 31) / 32};
@@ -640,9 +648,11 @@ int tile_rows(int d_out, int lpr, int* rpt_out) {
 
 using AggFn = void (*)(const int*, const int*, const float*, const int*, int, const float4*, int, int, float4*, int,
                        int, int*);
+#define GCNB_AGG_EXTRA_CASES(M) M(4, 3) M(8, 2) M(8, 4) M(16, 2)
 AggFn pick_agg(AggShape s) {
 #define M(L, V) if (s.lpr == L && s.vpl == V) return k_agg<L, V>;
   GCNB_LPR_CASES(M)
+  GCNB_AGG_EXTRA_CASES(M)
 #undef M
   return nullptr;
 }
@@ -722,9 +732,11 @@ int check_csr_args(const int32_t* row_ptr, const int32_t* col, const float* val,
 int launch_agg(const int32_t* row_ptr, const int32_t* col, const float* val, const int32_t* rows, int32_t n_rows,
                const float* x, int32_t ldx, int32_t d, float* y, int32_t ldy, int32_t act, cudaStream_t st,
                const char* what) {
-  const AggShape s = agg_shape(d);
+  AggShape s = agg_shape(d);
+  if (g_agg_lpr > 0 && g_agg_lpr * g_agg_vpl * 4 >= round4(d)) s = {g_agg_lpr, g_agg_vpl};
   AggFn fn = pick_agg(s);
-  const size_t smem = (size_t)WARPS * std::min(s.lpr, 8) * s.vpl * 32 * sizeof(float4);
+  GCNB_REQUIRE(fn != nullptr, "%s: no aggregation kernel for lpr=%d vpl=%d", what, s.lpr, s.vpl);
+  const size_t smem = (size_t)WARPS * agg_batch(s.lpr, s.vpl) * s.vpl * 32 * sizeof(float4);
   const int rows_per_block = NT / s.lpr;
   int per_sm = 0;
   if (smem > 48 * 1024) cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
@@ -764,6 +776,15 @@ int launch_fwd_gemm(bool agg, const int32_t* row_ptr, const int32_t* col, const 
 }  // namespace gcnb
 
 using namespace gcnb;
+
+extern "C" int gcnb_set_agg_shape(int32_t lpr, int32_t vpl) {
+  GCNB_REQUIRE((lpr == 0 && vpl == 0) || (lpr >= 2 && lpr <= 32 && vpl >= 1 && vpl <= 4),
+               "agg shape: lpr in [2, 32], vpl in [1, 4] (or 0, 0 = auto)");
+  if (lpr && !pick_agg({lpr, vpl})) return set_error(GCNB_EINVAL, "agg shape (%d, %d) not instantiated", lpr, vpl);
+  g_agg_lpr = lpr;
+  g_agg_vpl = vpl;
+  return GCNB_OK;
+}
 
 extern "C" int gcnb_spmm_f32(const int32_t* row_ptr, const int32_t* col, const float* val, const int32_t* rows,
                              int32_t n_rows, const float* x, int32_t ldx, int32_t d, float* y, int32_t ldy,
