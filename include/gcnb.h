@@ -136,6 +136,9 @@ int gcnb_set_dense_mode(int32_t mode);
 /* Test/tuning knob: force the (lanes per row, float4 chunks per lane) shape of
  * the aggregation kernel for every width it covers (0, 0 = automatic). */
 int gcnb_set_agg_shape(int32_t lpr, int32_t vpl);
+/* Test/tuning knob: gathers of the aggregation kernel staged through shared
+ * memory with cp.async (0, default) or batched in registers (1). */
+int gcnb_set_agg_gather(int32_t mode);
 
 /* runtime._bwd_compute (runtime.py:344-356) for the row list `rows`:
  *   agg[r]   = A_back[r,:]·G                       (G extended, d_k wide)

@@ -208,7 +208,8 @@ template <int LPR, int VPL>
 __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const int* __restrict__ col,
                                             const float* __restrict__ val, const int* __restrict__ rows,
                                             int n_rows, const float4* __restrict__ X4, int ldx4, int c4,
-                                            float4* __restrict__ Y4, int ldy4, int act, int* __restrict__ sched) {
+                                            float4* __restrict__ Y4, int ldy4, int act, int* __restrict__ sched,
+                                            int regs) {
   constexpr int GPW = 32 / LPR;
   constexpr int CH = AGG_ROWS_PER_GRAB > GPW ? AGG_ROWS_PER_GRAB / GPW : 1;  // row groups per grab
   constexpr int RPG = GPW * CH;                                                // rows per grab
@@ -246,7 +247,8 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
     float4 acc[VPL];
 #pragma unroll
     for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    aggregate_span_cp<LPR, VPL, U>(col, val, s, len, X4, ldx4, c4, gl, acc, stage);
+    if (regs) aggregate_span<LPR, VPL>(col, val, s, len, X4, ldx4, c4, gl, acc);
+    else aggregate_span_cp<LPR, VPL, U>(col, val, s, len, X4, ldx4, c4, gl, acc, stage);
     if (row >= 0) {
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
@@ -611,6 +613,7 @@ struct AggShape {
 
 // Forced (lpr, vpl) for the aggregation-only kernel (gcnb_set_agg_shape; 0 = auto).
 int g_agg_lpr = 0, g_agg_vpl = 0;
+int g_agg_regs = 0;  // 1: register-batched gathers instead of cp.async staging (gcnb_set_agg_gather)
 
 AggShape agg_shape(int d) {
   const int c4 = round4(d) / 4;
@@ -647,7 +650,7 @@ int tile_rows(int d_out, int lpr, int* rpt_out) {
 #define GCNB_LPR_CASES(M) M(2, 1) M(4, 1) M(8, 1) M(16, 1) M(32, 1) M(32, 2)
 
 using AggFn = void (*)(const int*, const int*, const float*, const int*, int, const float4*, int, int, float4*, int,
-                       int, int*);
+                       int, int*, int);
 #define GCNB_AGG_EXTRA_CASES(M) M(4, 3) M(8, 2) M(8, 4) M(16, 2)
 AggFn pick_agg(AggShape s) {
 #define M(L, V) if (s.lpr == L && s.vpl == V) return k_agg<L, V>;
@@ -750,7 +753,7 @@ int launch_agg(const int32_t* row_ptr, const int32_t* col, const float* val, con
   int* sched = sched_counter(st);
   GCNB_REQUIRE(sched != nullptr, "%s: no work-counter slot for this stream", what);
   fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, reinterpret_cast<const float4*>(x), ldx / 4,
-                             round4(d) / 4, reinterpret_cast<float4*>(y), ldy / 4, act, sched);
+                             round4(d) / 4, reinterpret_cast<float4*>(y), ldy / 4, act, sched, g_agg_regs);
   GCNB_AFTER_LAUNCH(what);
   return GCNB_OK;
 }
@@ -783,6 +786,12 @@ extern "C" int gcnb_set_agg_shape(int32_t lpr, int32_t vpl) {
   if (lpr && !pick_agg({lpr, vpl})) return set_error(GCNB_EINVAL, "agg shape (%d, %d) not instantiated", lpr, vpl);
   g_agg_lpr = lpr;
   g_agg_vpl = vpl;
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_set_agg_gather(int32_t mode) {
+  GCNB_REQUIRE(mode == 0 || mode == 1, "agg gather mode: 0 (cp.async staging) or 1 (register batches)");
+  g_agg_regs = mode;
   return GCNB_OK;
 }
 

@@ -15,7 +15,8 @@ import paper_2212_05009_b200 as gb  # noqa: E402
 from paper_2212_05009_b200 import _lib, devmem  # noqa: E402
 
 wl_name = sys.argv[1] if len(sys.argv) > 1 else "products"
-cases = [tuple(int(v) for v in c.split(":")) for c in sys.argv[2:]] or [(48, 0, 0), (104, 0, 0)]
+cases = [tuple(int(v) for v in c.split(":")) for c in sys.argv[2:]] or [(48, 0, 0, 0), (104, 0, 0, 0)]
+cases = [c + (0,) * (4 - len(c)) for c in cases]  # d:lpr:vpl[:regs]
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(dev)
 wl = bench.build_workload(wl_name, 0)
@@ -25,11 +26,12 @@ op = states[0].op_fwd
 n, nnz = states[0].n_own, op.lay.nnz
 flush = torch.empty(512 * 1024 * 1024 // 4, device=dev)
 st = torch.cuda.current_stream(dev).cuda_stream
-for d, lpr, vpl in cases:
+for d, lpr, vpl, regs in cases:
     ld = devmem.feat_ld(d)
     x = torch.randn(n, ld, device=dev)
     y = torch.zeros(n, ld, device=dev)
     _lib.call("gcnb_set_agg_shape", lpr, vpl)
+    _lib.call("gcnb_set_agg_gather", regs)
     fn = lambda: _lib.call("gcnb_spmm_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(), op.csr.val.data_ptr(),
                            None, n, x.data_ptr(), ld, d, y.data_ptr(), ld, st)
     fn()
@@ -46,7 +48,8 @@ for d, lpr, vpl in cases:
     ms = min(ts)
     algo = 4 * (n + 1) + 8 * nnz + 4 * d * nnz + 4 * d * n
     same = bool(torch.equal(y, ref))
-    print(f"spmm d={d} lpr={lpr} vpl={vpl}: {ms:.3f} ms  {algo / ms / 1e6:.0f} GB/s (algorithmic)  rerun-identical={same}",
+    print(f"spmm d={d} lpr={lpr} vpl={vpl} regs={regs}: {ms:.3f} ms  {algo / ms / 1e6:.0f} GB/s (algorithmic)  rerun-identical={same}",
           flush=True)
     del x, y
 _lib.call("gcnb_set_agg_shape", 0, 0)
+_lib.call("gcnb_set_agg_gather", 0)
