@@ -164,6 +164,14 @@ int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, const float* 
  * partial blocks (d_prev*ld_k floats each) like gcnb_bwd_layer_f32. */
 int gcnb_dw_f32(const float* x, int32_t ldx, int32_t d_prev, const float* a, int32_t lda, int32_t d_k,
                 const int32_t* rows, int32_t n_rows, float* dw_partials, void* stream);
+/* The dense part of gcnb_bwd_layer_f32 from an aggregate already resident in
+ * `agg` (rows at own-row positions, e.g. gathered by gcnb_spmm_f32 for the
+ * interior and boundary row lists of an overlapped exchange): G_prev and the
+ * ΔW partials for the row list, gcnb_bwd_grid(n_rows, d_prev, d_k, g_prev != 0)
+ * partial blocks. */
+int gcnb_bwd_epilogue_f32(const float* agg, int32_t ldagg, int32_t d_k, const float* h_prev, int32_t ldhp,
+                          int32_t d_prev, const float* w, float* g_prev, int32_t ldgp, int32_t act,
+                          const int32_t* rows, int32_t n_rows, float* dw_partials, void* stream);
 /* Row stride (floats) of the optional `workspace` of gcnb_bwd_layer_f32 for
  * these widths, or 0 when the fused single-kernel form is always used.  With a
  * workspace of (own rows) × ld floats, large-ΔW layers run as an aggregation

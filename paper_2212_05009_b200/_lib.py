@@ -52,6 +52,8 @@ _SIGNATURES = {
     "gcnb_bwd_grid": (_c_int, [_c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_int)]),
     "gcnb_set_agg_shape": (_c_int, [_c_int, _c_int]),
     "gcnb_set_agg_gather": (_c_int, [_c_int]),
+    "gcnb_bwd_epilogue_f32": (_c_int, [_vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp,
+                                       _c_int, _vp, _vp]),
     "gcnb_dw_f32": (_c_int, [_vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp, _vp]),
     "gcnb_bwd_layer_f32": (
         _c_int,

@@ -726,6 +726,26 @@ int bwd_plan(int n_rows, int d_prev, int d_k, bool with_gp, BwdPlan* out) {
   return GCNB_OK;
 }
 
+// Dense part of the backward layer from a resident aggregate: G_prev =
+// (agg·Wᵀ) ⊙ σ'(H_prev) (when g_prev) and the ΔW partials H_prevᵀ·agg, on the
+// tcgen05 engines where they apply, else the SIMT backward kernel without CSR.
+int launch_bwd_epilogue(const float* agg, int ldagg, int d_k, const float* h_prev, int ldhp, int d_prev,
+                        const float* w, float* g_prev, int ldgp, int act, const int32_t* rows, int n_rows,
+                        float* dw_partials, const BwdPlan& plan, cudaStream_t st) {
+  if (dw_tc_applies(d_prev, d_k) && (!g_prev || dense_tc_applies(d_k, d_prev))) {
+    if (g_prev) {
+      if (int rc = launch_dense_tc(agg, ldagg, rows, n_rows, d_k, nullptr, d_prev, g_prev, ldgp, act, st, w,
+                                   round4(d_k), h_prev, ldhp))
+        return rc;
+    }
+    return launch_dw_tc(h_prev, ldhp, d_prev, agg, ldagg, d_k, rows, n_rows, dw_partials, plan.grid, st);
+  }
+  plan.fn<<<plan.grid, NT, plan.smem, st>>>(nullptr, nullptr, nullptr, rows, n_rows, agg, ldagg, d_k, h_prev, ldhp,
+                                            d_prev, w, g_prev, ldgp, act, dw_partials, plan.T);
+  GCNB_AFTER_LAUNCH("bwd layer (dense epilogue)");
+  return GCNB_OK;
+}
+
 int check_csr_args(const int32_t* row_ptr, const int32_t* col, const float* val, int32_t n_rows) {
   GCNB_REQUIRE(n_rows >= 0, "n_rows must be >= 0");
   GCNB_REQUIRE(n_rows == 0 || (row_ptr && col && val), "CSR arrays must be non-null");
@@ -876,19 +896,8 @@ extern "C" int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
     if (int rc = launch_agg(row_ptr, col, val, rows, n_rows, g, ldg, d_k, workspace, round4(d_k), -1, st,
                             "bwd layer (aggregate)"))
       return rc;
-    if (dw_tc_applies(d_prev, d_k) && (!g_prev || dense_tc_applies(d_k, d_prev))) {
-      // tensor-core epilogue: G_prev = (agg·Wᵀ) ⊙ σ'(H_prev) and the ΔW partials, 3xTF32
-      if (g_prev) {
-        if (int rc = launch_dense_tc(workspace, round4(d_k), rows, n_rows, d_k, nullptr, d_prev, g_prev, ldgp, act, st,
-                                     w, round4(d_k), h_prev, ldhp))
-          return rc;
-      }
-      return launch_dw_tc(h_prev, ldhp, d_prev, workspace, round4(d_k), d_k, rows, n_rows, dw_partials, plan.grid, st);
-    }
-    plan.fn<<<plan.grid, NT, plan.smem, st>>>(nullptr, nullptr, nullptr, rows, n_rows, workspace, round4(d_k), d_k,
-                                              h_prev, ldhp, d_prev, w, g_prev, ldgp, act, dw_partials, plan.T);
-    GCNB_AFTER_LAUNCH("bwd layer (dense epilogue)");
-    return GCNB_OK;
+    return launch_bwd_epilogue(workspace, round4(d_k), d_k, h_prev, ldhp, d_prev, w, g_prev, ldgp, act, rows, n_rows,
+                               dw_partials, plan, st);
   }
   plan.fn<<<plan.grid, NT, plan.smem, st>>>(row_ptr, col, val, rows, n_rows, g, ldg, d_k, h_prev, ldhp, d_prev, w,
                                             g_prev, ldgp, act, dw_partials, plan.T);
@@ -914,6 +923,26 @@ extern "C" int gcnb_dw_f32(const float* x, int32_t ldx, int32_t d_prev, const fl
                                             nullptr, nullptr, 0, GCNB_ACT_IDENTITY, dw_partials, plan.T);
   GCNB_AFTER_LAUNCH("dw");
   return GCNB_OK;
+}
+
+extern "C" int gcnb_bwd_epilogue_f32(const float* agg, int32_t ldagg, int32_t d_k, const float* h_prev,
+                                     int32_t ldhp, int32_t d_prev, const float* w, float* g_prev, int32_t ldgp,
+                                     int32_t act, const int32_t* rows, int32_t n_rows, float* dw_partials,
+                                     void* stream) {
+  GCNB_REQUIRE(n_rows >= 0, "bwd epilogue: n_rows must be >= 0");
+  GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "bwd epilogue: unknown activation %d", act);
+  GCNB_REQUIRE(d_prev >= 1 && d_prev <= 256 && d_k >= 1 && d_k <= 256, "bwd epilogue: widths out of range");
+  GCNB_REQUIRE(ldagg % 4 == 0 && ldhp % 4 == 0 && ldagg >= round4(d_k) && ldhp >= round4(d_prev),
+               "bwd epilogue: row strides must be multiples of 4 and cover the widths");
+  GCNB_REQUIRE(!g_prev || (ldgp % 4 == 0 && ldgp >= round4(d_prev) && aligned16(g_prev) && w && aligned16(w)),
+               "bwd epilogue: G_prev needs W and an aligned stride >= round4(d_prev)");
+  GCNB_REQUIRE(agg && h_prev && dw_partials && aligned16(agg) && aligned16(h_prev) && aligned16(dw_partials),
+               "bwd epilogue: operands must be non-null and 16-byte aligned");
+  BwdPlan plan;
+  if (int rc = bwd_plan(n_rows, d_prev, d_k, g_prev != nullptr, &plan)) return rc;
+  if (n_rows == 0) return GCNB_OK;
+  return launch_bwd_epilogue(agg, ldagg, d_k, h_prev, ldhp, d_prev, w, g_prev, ldgp, act, rows, n_rows, dw_partials,
+                             plan, (cudaStream_t)stream);
 }
 
 extern "C" int gcnb_bwd_workspace_ld(int32_t d_prev, int32_t d_k, int32_t* ld_out) {

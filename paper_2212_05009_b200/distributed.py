@@ -319,6 +319,8 @@ class DistributedTrainer:
             if comm:
                 self._wait(self.flags_halo, self.expected_halo, self.sched.fwd_src, f"wait_fwd{k}")
             st.fwd_compute(k, "boundary" if self.overlap else "all")
+            if self.overlap:
+                st.fwd_finish(k)
         st.loss_grad(1.0 / self.n_lab)
         for k in range(L, 0, -1):
             if st.skips_bwd_exchange(k):
@@ -331,7 +333,10 @@ class DistributedTrainer:
                 if comm:
                     self._wait(self.flags_halo, self.expected_halo, self.sched.bwd_src, f"wait_bwd{k}")
                 gb = st.bwd_compute(k, "boundary", slot=gi)
-                st.reduce_dw(k, gi + gb)
+                if st.bwd_split(k):
+                    st.reduce_dw(k, st.bwd_finish(k))
+                else:
+                    st.reduce_dw(k, gi + gb)
             else:
                 if comm:
                     self._wait(self.flags_halo, self.expected_halo, self.sched.bwd_src, f"wait_bwd{k}")

@@ -424,17 +424,17 @@ class ProcState:
         d_out = self.dims[k]
         if fused and self.fwd_ws[k] is not None:
             # wide layer: the gather-bound aggregation runs alone at full
-            # occupancy (Y → workspace), then the dense transform streams Y
+            # occupancy (Y → workspace), then the dense transform streams Y.
+            # For an interior/boundary row list only the aggregation runs:
+            # fwd_finish(k) transforms all own rows at once (contiguous: TMA).
             ws = self.fwd_ws[k]
             with span(f"fwd{k}", 4 * (n_sel + 1) + 8 * nnz + 4 * width * nnz + 4 * width * n_sel, 2 * nnz * width,
                       self.stream()):
                 _lib.call("gcnb_fwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
                           op.csr.val.data_ptr(), sel, n_sel, x.data_ptr(), x.shape[1], width, 0, width,
                           ws.data_ptr(), ws.shape[1], _lib.ACT["identity"], self.stream())
-            with span(f"dense{k}", 4 * (n_sel * width + width * d_out + n_sel * d_out),
-                      2 * n_sel * width * d_out, self.stream()):
-                _lib.call("gcnb_dense_f32", ws.data_ptr(), ws.shape[1], sel, n_sel, width, w, d_out, h.data_ptr(),
-                          h.shape[1], self.act, self.stream())
+            if rows == "all":
+                self.fwd_finish(k)
             return
         algo = 4 * (n_sel + 1) + 8 * nnz + 4 * width * nnz + 4 * d_out * n_sel
         flops = 2 * nnz * width
@@ -445,6 +445,42 @@ class ProcState:
             _lib.call("gcnb_fwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
                       op.csr.val.data_ptr(), sel, n_sel, x.data_ptr(), x.shape[1], width, w, d_out, h.data_ptr(),
                       h.shape[1], self.act, self.stream())
+
+    def fwd_split(self, k: int) -> bool:
+        """Layer k's forward runs as aggregation + dense transform (fwd_finish)."""
+        return not self.transform_first[k] and self.fwd_ws[k] is not None
+
+    def fwd_finish(self, k: int) -> None:
+        """Dense transform H^k = act(Y·W^k) of all own rows from the workspace."""
+        if not self.fwd_split(k) or self.n_own == 0:
+            return
+        ws, h = self.fwd_ws[k], self.hbuf[k]
+        n, width, d_out = self.n_own, self.dims[k - 1], self.dims[k]
+        with span(f"dense{k}", 4 * (n * width + width * d_out + n * d_out), 2 * n * width * d_out, self.stream()):
+            _lib.call("gcnb_dense_f32", ws.data_ptr(), ws.shape[1], None, n, width, self.w[k].data_ptr(), d_out,
+                      h.data_ptr(), h.shape[1], self.act, self.stream())
+
+    def bwd_split(self, k: int) -> bool:
+        """Layer k's backward runs as aggregation + dense epilogue (bwd_finish)."""
+        return self.bwd_ws[k] is not None
+
+    def bwd_finish(self, k: int) -> int:
+        """G^{k-1} and the ΔW^k partials of all own rows from the aggregate in the
+        workspace (after interior/boundary aggregations); returns slots used."""
+        ws = self.bwd_ws[k]
+        hp = self.hbuf[k - 1]
+        gp = self.gext[k - 1] if k > 1 else None
+        dk, dp = self.dims[k], self.dims[k - 1]
+        n = self.n_own
+        used = self.bwd_grids[k][2]
+        if n == 0:
+            return 0
+        algo = 4 * n * (dk + 2 * dp) + 4 * dp * dk * used + (4 * dp * n if gp is not None else 0)
+        with span(f"bwd{k}", algo, 2 * n * dp * dk * (2 if gp is not None else 1), self.stream()):
+            _lib.call("gcnb_bwd_epilogue_f32", ws.data_ptr(), ws.shape[1], dk, hp.data_ptr(), hp.shape[1], dp,
+                      self.w[k].data_ptr(), 0 if gp is None else gp.data_ptr(), 0 if gp is None else gp.shape[1],
+                      self.act, None, n, self.partials[k].data_ptr(), self.stream())
+        return used
 
     def loss_grad(self, inv_n_labeled: float) -> None:
         """runtime._local_loss_grad: loss_sum and G^L for own rows."""
@@ -463,6 +499,16 @@ class ProcState:
         gi, gb, ga = self.bwd_grids[k]
         used = {"all": ga, "interior": gi, "boundary": gb}[rows]
         g = self.gext[k]
+        if rows != "all" and self.bwd_split(k):
+            # row list of an overlapped exchange: aggregate only (bwd_finish does the rest)
+            op_nnz = op.nnz_of(rows)
+            ws = self.bwd_ws[k]
+            with span(f"bwd{k}", 4 * (n_sel + 1) + 8 * op_nnz + 4 * self.dims[k] * (op_nnz + n_sel), 2 * op_nnz *
+                      self.dims[k], self.stream()):
+                _lib.call("gcnb_spmm_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(), op.csr.val.data_ptr(),
+                          sel, n_sel, g.data_ptr(), g.shape[1], self.dims[k], ws.data_ptr(), ws.shape[1],
+                          self.stream())
+            return 0
         hp = self.hbuf[k - 1]
         gp = self.gext[k - 1] if k > 1 else None
         part = self.partials[k][slot:]
