@@ -270,6 +270,21 @@ def roofline_summary(kernel_rows, peak, peak_kind, steps):
     return name, achieved, mean_ms, algo // cnt, table
 
 
+def roofline_line(kname, achieved, peak, peak_kind, traffic, kbytes, kms):
+    """`achieved` counts ALGORITHMIC bytes (every gathered neighbour row, no cache
+    reuse), so an L2-resident gather stream reads above the HBM copy peak; the
+    ncu DRAM bytes of the same kernel (`traffic`, profiles/traffic.json) give the
+    HBM side: traffic_gbs = traffic / this run's launch time."""
+    line = {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic, "algo_bytes_per_launch": kbytes,
+            "ms_per_launch": round(kms, 5)}
+    if traffic:
+        line["traffic_gbs"] = round(traffic / (kms * 1e-3) / 1e9, 1)
+        line["traffic_frac"] = round(line["traffic_gbs"] / peak, 4)
+        line["l2_reuse"] = round(kbytes / traffic, 2)
+    return line
+
+
 def traffic_for(workload: str, kernel: str):
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
@@ -385,10 +400,7 @@ def run_single(args):
         "e2e": {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "loss_last": m[0].loss if m[0] is not None else None},
         "gpu_launches": int(launches_per_epoch * args.steps),
-        "roofline": {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": traffic_for(wl["name"], kname), "algo_bytes_per_launch": kbytes,
-                     "ms_per_launch": round(kms, 5)},
+        "roofline": roofline_line(kname, achieved, peak, peak_kind, traffic_for(wl["name"], kname), kbytes, kms),
         "kernels": table,
         "halo_bytes_per_epoch": 0, "exposed_comm_pct": 0.0,
         "cpu_baseline": {"value": round(cpu_ms, 3), "unit": UNIT, "cores": cpu_threads, "kind": "port",

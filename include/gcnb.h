@@ -133,6 +133,13 @@ int gcnb_dense_f32(const float* x, int32_t ldx, const int32_t* rows, int32_t n_r
  * everywhere, 2 = tcgen05 wherever the tile fits shared memory.  Both engines
  * meet the 1e-4 fp32 bar; they differ in the last bits. */
 int gcnb_set_dense_mode(int32_t mode);
+/* *out = 1 when the tcgen05 engine serves act(X·W) for these widths. */
+int gcnb_dense_tc_applies(int32_t d_in, int32_t d_out, int32_t* out);
+/* H = relu(X·W) over rows 0..n_rows-1 (tcgen05 engine only) and its sign bits:
+ * bit m of bits[r*ld_bits + m/32] = (H[r][m] > 0), i.e. σ'(Z) (gcn.py:101-104)
+ * for the backward mask at 1/32 of H's bytes.  ld_bits % 4 == 0. */
+int gcnb_dense_bits_f32(const float* x, int32_t ldx, int32_t n_rows, int32_t d_in, const float* w, int32_t d_out,
+                        float* y, int32_t ldy, uint32_t* bits, int32_t ld_bits, void* stream);
 /* Test/tuning knob: force the (lanes per row, float4 chunks per lane) shape of
  * the aggregation kernel for every width it covers (0, 0 = automatic). */
 int gcnb_set_agg_shape(int32_t lpr, int32_t vpl);
@@ -171,7 +178,10 @@ int gcnb_dw_f32(const float* x, int32_t ldx, int32_t d_prev, const float* a, int
  * partial blocks. */
 int gcnb_bwd_epilogue_f32(const float* agg, int32_t ldagg, int32_t d_k, const float* h_prev, int32_t ldhp,
                           int32_t d_prev, const float* w, float* g_prev, int32_t ldgp, int32_t act,
-                          const int32_t* rows, int32_t n_rows, float* dw_partials, void* stream);
+                          const uint32_t* hbits, int32_t ld_hbits, const int32_t* rows, int32_t n_rows,
+                          float* dw_partials, void* stream);
+/* (hbits, optional: sign bits of H_prev as written by gcnb_dense_bits_f32 — the
+ * G_prev mask then reads ld_hbits words per row instead of H_prev's floats.) */
 /* Row stride (floats) of the optional `workspace` of gcnb_bwd_layer_f32 for
  * these widths, or 0 when the fused single-kernel form is always used.  With a
  * workspace of (own rows) × ld floats, large-ΔW layers run as an aggregation

@@ -53,7 +53,9 @@ _SIGNATURES = {
     "gcnb_set_agg_shape": (_c_int, [_c_int, _c_int]),
     "gcnb_set_agg_gather": (_c_int, [_c_int]),
     "gcnb_bwd_epilogue_f32": (_c_int, [_vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp,
-                                       _c_int, _vp, _vp]),
+                                       _c_int, _vp, _c_int, _vp, _vp]),
+    "gcnb_dense_tc_applies": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_int)]),
+    "gcnb_dense_bits_f32": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp, _c_int, _vp, _c_int, _vp]),
     "gcnb_dw_f32": (_c_int, [_vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp, _vp]),
     "gcnb_bwd_layer_f32": (
         _c_int,
@@ -139,6 +141,12 @@ def int_array(vals) -> ctypes.Array:
 
 def launch_count() -> int:
     return int(load().gcnb_launch_count())
+
+
+def dense_tc_applies(d_in: int, d_out: int) -> bool:
+    out = _c_int(0)
+    call("gcnb_dense_tc_applies", d_in, d_out, ctypes.byref(out))
+    return bool(out.value)
 
 
 def bwd_grid(n_rows: int, d_prev: int, d_k: int, with_gprev: bool) -> int:

@@ -35,9 +35,13 @@ int launch_dense_blocked(const float* x, int ldx, const int* rows, int n_rows, i
 bool dense_tc_applies(int d_in, int d_out);
 // w_nk != nullptr: B = w_nk stored N×K (row stride ld_wnk) instead of w (K×N);
 // hmask != nullptr: epilogue y = acc ⊙ σ'(hmask) (backward) instead of act(acc)
+// hbits != nullptr: the mask comes from packed sign bits (ld_hbits words per
+// row) instead of hmask; bits_out != nullptr (unmasked ReLU): also write the
+// sign bits of the output (ld_bits_out words per row) for the backward pass.
 int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
                     float* y, int ldy, int act, cudaStream_t st, const float* w_nk = nullptr, int ld_wnk = 0,
-                    const float* hmask = nullptr, int ldhm = 0);
+                    const float* hmask = nullptr, int ldhm = 0, const uint32_t* hbits = nullptr, int ld_hbits = 0,
+                    uint32_t* bits_out = nullptr, int ld_bits_out = 0);
 bool dw_tc_applies(int d_prev, int d_k);
 int dw_tc_grid(int n_rows);
 int launch_dw_tc(const float* h, int ldh, int d_prev, const float* a, int lda, int d_k, const int* rows, int n_rows,

@@ -208,12 +208,16 @@ __device__ __forceinline__ void load_mask_rows(uint32_t stage, const float* __re
 // SWIZZLE_128B boxes of 32 floats × NT_ rows (out-of-range K and rows arrive
 // as zeros) plus, masked, one box of the mask rows; completion is counted by
 // the stage's mbarrier (expect_tx), so loads run up to S tiles ahead.
-template <bool RELU, bool MASKED, bool TMA>
+// MK (mask kind): 0 act(X·W); 1 ⊙σ'(Hm) with Hm fp32 rows (ldhm floats);
+// 2 ⊙σ'(H) from packed sign bits (Hm = uint32 words, ldhm words per row, bit m
+// of word m/32 = (H[m] > 0)), which the forward writes through `bits_out`.
+template <bool RELU, int MK, bool TMA>
 __global__ void __launch_bounds__(DT_THREADS, 1)
     k_dense_tc(const float* __restrict__ X, int ldx, const int* __restrict__ rows, int n_rows, int K,
                const float* __restrict__ W, int ldw, int w_nk, int M, int NT_, int S, float* __restrict__ Y,
-               int ldy, const float* __restrict__ Hm, int ldhm, const __grid_constant__ CUtensorMap tmx,
-               const __grid_constant__ CUtensorMap tmm) {
+               int ldy, const float* __restrict__ Hm, int ldhm, uint32_t* __restrict__ bits_out, int ld_bits,
+               const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmm) {
+  constexpr bool MASKED = MK != 0;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[4 * DT_MAX_STAGES + 4];
   __shared__ uint32_t tmem_base_slot;
@@ -221,7 +225,8 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
   const int Kb = (K + 31) & ~31;                  // smem K extent (whole 128-byte swizzle lines)
   const int mpad = (M + 3) & ~3;                  // mask tile row stride (floats)
   const uint32_t x_bytes = (uint32_t)NT_ * Kb * 4;
-  const uint32_t m_bytes = MASKED ? (uint32_t)NT_ * mpad * 4 : 0;
+  const int mrow = MK == 2 ? ldhm : mpad;           // mask tile row: floats (MK 1) or words (MK 2)
+  const uint32_t m_bytes = MASKED ? (uint32_t)NT_ * mrow * 4 : 0;
   const uint32_t st_bytes = (x_bytes + m_bytes + 1023) & ~1023u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (n_rows + NT_ - 1) / NT_;
@@ -293,7 +298,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
   if (TMA && warp >= 8 && warp < 12) {
     // ---------------- producer (TMA)
     if (warp == 8 && lane == 0) {
-      const uint32_t tx = (uint32_t)(Kb / 32) * NT_ * 128 + (MASKED ? (uint32_t)NT_ * mpad * 4 : 0u);
+      const uint32_t tx = (uint32_t)(Kb / 32) * NT_ * 128 + m_bytes;
       int t = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
         const int s = t % S;
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
       if (t >= S) mbar_wait(bar(3, s), (uint32_t)(t / S - 1) & 1u);
       const uint32_t st = smem_u32(smem + s * st_bytes);
       load_x_rows(st, X, ldx, rows, n_rows, tile * NT_, NT_, kc, tid);
-      if (MASKED) load_mask_rows(st + x_bytes, Hm, ldhm, rows, n_rows, tile * NT_, NT_, mpad, tid);
+      if (MASKED) load_mask_rows(st + x_bytes, Hm, ldhm, rows, n_rows, tile * NT_, NT_, mrow, tid);
       asm volatile("cp.async.commit_group;" ::: "memory");
       if (t >= 1) {
         asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -396,6 +401,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
       if (MASKED) mbar_wait(bar(0, s), (uint32_t)(t / S) & 1u);
       tc_after_sync();
       const float* ms = reinterpret_cast<const float*>(smem + s * st_bytes + x_bytes);
+      const uint32_t* mw = reinterpret_cast<const uint32_t*>(ms);
       const int i0 = tile * NT_;
       for (int n0 = hs * span; n0 < (hs + 1) * span && i0 + n0 < n_rows; n0 += 16) {
         uint32_t v[16];
@@ -410,12 +416,26 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           o[j] = __uint_as_float(v[j]);
-          if (MASKED) {
+          if (MK == 1) {
             const float hv = m_mask ? ms[(n0 + j) * mpad + m] : 1.0f;
             o[j] = RELU ? (hv > 0.0f ? o[j] : 0.0f) : o[j];
+          } else if (MK == 2) {
+            const uint32_t w = mw[(n0 + j) * ldhm + q];
+            o[j] = RELU ? (((w >> lane) & 1u) ? o[j] : 0.0f) : o[j];
           } else if (RELU) {
             o[j] = fmaxf(o[j], 0.0f);
           }
+        }
+        if (MK == 0 && RELU && bits_out != nullptr) {
+          // σ' of this layer's output for the backward pass: one ballot per row
+          uint32_t mine = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const uint32_t bw = __ballot_sync(0xffffffffu, o[j] > 0.0f);
+            if (lane == j) mine = bw;
+          }
+          const int i = i0 + n0 + lane;
+          if (lane < 16 && i < n_rows) bits_out[(size_t)(rows ? __ldg(rows + i) : i) * ld_bits + q] = mine;
         }
         if (!m_out) continue;
         if (rows == nullptr && i0 + n0 + 16 <= n_rows) {
@@ -450,13 +470,17 @@ constexpr size_t DT_SMEM_MAX = 227 * 1024 - 1024;
 // tile t to drain (lo MMAs of tile t-S), while the MMA issuer needs tile t-1
 // before it issues those lo MMAs of tile t-2 — with S = 2 that is a cycle.
 // TMA completion does not wait on later tiles, so two suffice there.
-int dense_tc_tile(int d_in, int d_out, bool masked, bool tma, int* stages, size_t* smem_out) {
+// mask_row: floats (or bit words) of the mask tile per row, 0 when unmasked.
+int dense_tc_tile(int d_in, int d_out, int mask_row, bool tma, int* stages, size_t* smem_out) {
   if (d_in > 128 || d_out > 128) return 0;  // Wᵀ hi+lo ≤ 256 TMEM columns; one 128-lane half
-  const int Kb = (d_in + 31) & ~31, mpad = (d_out + 3) & ~3;
+  const bool masked = mask_row > 0;
+  const int Kb = (d_in + 31) & ~31;
   for (int nt = 128; nt >= 32; nt >>= 1) {
-    const size_t st = ((size_t)nt * (Kb + (masked ? mpad : 0)) * 4 + 1023) & ~(size_t)1023;
+    const size_t st = ((size_t)nt * (Kb + mask_row) * 4 + 1023) & ~(size_t)1023;
     const int s = (int)std::min<size_t>(DT_MAX_STAGES, DT_SMEM_MAX / st);
-    if (s >= (tma ? 2 : 3)) {
+    // masked: the epilogue releases a stage only after reading its mask rows,
+    // so two stages would serialise load, MMA and epilogue — keep three
+    if (s >= (tma && !masked ? 2 : 3)) {
       *stages = s;
       *smem_out = s * st;
       return nt;
@@ -471,7 +495,7 @@ bool dense_tc_applies(int d_in, int d_out) {
   int stages = 0;
   size_t smem = 0;
   // the backward form carries a mask tile: require that it fits too
-  const bool fits = dense_tc_tile(d_in, d_out, true, false, &stages, &smem) > 0;
+  const bool fits = dense_tc_tile(d_in, d_out, (d_out + 3) & ~3, false, &stages, &smem) > 0;
   if (g_dense_mode == 2) return fits;
   return fits && d_in >= 32 && d_out >= 32;
 }
@@ -514,36 +538,44 @@ bool tmap_2d(CUtensorMap* m, const float* base, int cols, int n_rows, int ld, in
 
 int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
                     float* y, int ldy, int act, cudaStream_t st, const float* w_nk, int ld_wnk, const float* hmask,
-                    int ldhm) {
-  const bool masked = hmask != nullptr;
+                    int ldhm, const uint32_t* hbits, int ld_hbits, uint32_t* bits_out, int ld_bits_out) {
+  const int mk = hbits ? 2 : hmask ? 1 : 0;
   const int mpad = (d_out + 3) & ~3;
+  const int mask_row = mk == 2 ? ld_hbits : mk == 1 ? mpad : 0;
+  const float* mptr = mk == 2 ? reinterpret_cast<const float*>(hbits) : hmask;
+  const int mld = mk == 2 ? ld_hbits : ldhm;
+  GCNB_REQUIRE(mk != 1 || ldhm >= mpad, "dense (tcgen05): mask stride too small");
+  GCNB_REQUIRE(mk != 2 || (ld_hbits % 4 == 0 && ld_hbits * 32 >= d_out), "dense (tcgen05): mask-bit stride");
+  GCNB_REQUIRE(!bits_out || (act == GCNB_ACT_RELU && mk == 0 && ld_bits_out * 32 >= d_out),
+               "dense (tcgen05): sign bits are written for an unmasked ReLU transform only");
   CUtensorMap tmx, tmm;
   std::memset(&tmx, 0, sizeof(tmx));
   std::memset(&tmm, 0, sizeof(tmm));
   int stages = 0;
   size_t smem = 0;
   bool tma = rows == nullptr && n_rows > 0;
-  int nt = tma ? dense_tc_tile(d_in, d_out, masked, true, &stages, &smem) : 0;
+  int nt = tma ? dense_tc_tile(d_in, d_out, mask_row, true, &stages, &smem) : 0;
   if (tma) {
     tma = nt > 0 && tmap_2d(&tmx, x, d_in, n_rows, ldx, 32, nt, CU_TENSOR_MAP_SWIZZLE_128B) &&
-          (!masked || tmap_2d(&tmm, hmask, mpad, n_rows, ldhm, mpad, nt, CU_TENSOR_MAP_SWIZZLE_NONE));
+          (mk == 0 || tmap_2d(&tmm, mptr, mask_row, n_rows, mld, mask_row, nt, CU_TENSOR_MAP_SWIZZLE_NONE));
   }
-  if (!tma) nt = dense_tc_tile(d_in, d_out, masked, false, &stages, &smem);
+  if (!tma) nt = dense_tc_tile(d_in, d_out, mask_row, false, &stages, &smem);
   GCNB_REQUIRE(nt > 0, "dense (tcgen05): widths %d -> %d not supported", d_in, d_out);
-  GCNB_REQUIRE(!hmask || ldhm >= mpad, "dense (tcgen05): mask stride too small");
   const bool relu = act == GCNB_ACT_RELU;
   using Fn = void (*)(const float*, int, const int*, int, int, const float*, int, int, int, int, int, float*, int,
-                      const float*, int, const CUtensorMap, const CUtensorMap);
-  Fn fn;
-  if (tma) fn = masked ? (relu ? k_dense_tc<true, true, true> : k_dense_tc<false, true, true>)
-                       : (relu ? k_dense_tc<true, false, true> : k_dense_tc<false, false, true>);
-  else fn = masked ? (relu ? k_dense_tc<true, true, false> : k_dense_tc<false, true, false>)
-                   : (relu ? k_dense_tc<true, false, false> : k_dense_tc<false, false, false>);
+                      const float*, int, uint32_t*, int, const CUtensorMap, const CUtensorMap);
+#define GCNB_DT_PICK(T)                                                                              \
+  (mk == 2 ? (relu ? k_dense_tc<true, 2, T> : k_dense_tc<false, 2, T>)                               \
+           : mk == 1 ? (relu ? k_dense_tc<true, 1, T> : k_dense_tc<false, 1, T>)                     \
+                     : (relu ? k_dense_tc<true, 0, T> : k_dense_tc<false, 0, T>))
+  Fn fn = tma ? GCNB_DT_PICK(true) : GCNB_DT_PICK(false);
+#undef GCNB_DT_PICK
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles = (n_rows + nt - 1) / nt;
   const int grid = std::max(1, std::min(tiles, num_sms()));
   fn<<<grid, DT_THREADS, smem, st>>>(x, ldx, rows, n_rows, d_in, w_nk ? w_nk : w, w_nk ? ld_wnk : round4(d_out),
-                                     w_nk ? 1 : 0, d_out, nt, stages, y, ldy, hmask, ldhm, tmx, tmm);
+                                     w_nk ? 1 : 0, d_out, nt, stages, y, ldy, mptr, mld, bits_out, ld_bits_out, tmx,
+                                     tmm);
   GCNB_AFTER_LAUNCH(tma ? "dense (tcgen05 3xTF32, TMA)" : "dense (tcgen05 3xTF32)");
   return GCNB_OK;
 }

@@ -731,11 +731,12 @@ int bwd_plan(int n_rows, int d_prev, int d_k, bool with_gp, BwdPlan* out) {
 // tcgen05 engines where they apply, else the SIMT backward kernel without CSR.
 int launch_bwd_epilogue(const float* agg, int ldagg, int d_k, const float* h_prev, int ldhp, int d_prev,
                         const float* w, float* g_prev, int ldgp, int act, const int32_t* rows, int n_rows,
-                        float* dw_partials, const BwdPlan& plan, cudaStream_t st) {
+                        float* dw_partials, const BwdPlan& plan, cudaStream_t st, const uint32_t* hbits = nullptr,
+                        int ld_hbits = 0) {
   if (dw_tc_applies(d_prev, d_k) && (!g_prev || dense_tc_applies(d_k, d_prev))) {
     if (g_prev) {
       if (int rc = launch_dense_tc(agg, ldagg, rows, n_rows, d_k, nullptr, d_prev, g_prev, ldgp, act, st, w,
-                                   round4(d_k), h_prev, ldhp))
+                                   round4(d_k), h_prev, ldhp, hbits, ld_hbits))
         return rc;
     }
     return launch_dw_tc(h_prev, ldhp, d_prev, agg, ldagg, d_k, rows, n_rows, dw_partials, plan.grid, st);
@@ -863,6 +864,29 @@ extern "C" int gcnb_dense_f32(const float* x, int32_t ldx, const int32_t* rows, 
                          (cudaStream_t)stream, "dense");
 }
 
+extern "C" int gcnb_dense_tc_applies(int32_t d_in, int32_t d_out, int32_t* out) {
+  GCNB_REQUIRE(out != nullptr, "dense tc applies: null output");
+  *out = dense_tc_applies(d_in, d_out) ? 1 : 0;
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_dense_bits_f32(const float* x, int32_t ldx, int32_t n_rows, int32_t d_in, const float* w,
+                                   int32_t d_out, float* y, int32_t ldy, uint32_t* bits, int32_t ld_bits,
+                                   void* stream) {
+  GCNB_REQUIRE(n_rows >= 0, "dense bits: n_rows must be >= 0");
+  GCNB_REQUIRE(d_in >= 1 && d_in <= 256 && d_out >= 1 && d_out <= 256, "dense bits: widths out of range");
+  GCNB_REQUIRE(ldx % 4 == 0 && ldy % 4 == 0 && ldx >= round4(d_in) && ldy >= round4(d_out),
+               "dense bits: row strides must be multiples of 4 and cover the widths");
+  GCNB_REQUIRE(x && w && y && bits && aligned16(x) && aligned16(w) && aligned16(y) && aligned16(bits),
+               "dense bits: operands must be non-null and 16-byte aligned");
+  GCNB_REQUIRE(ld_bits % 4 == 0 && ld_bits * 32 >= d_out, "dense bits: bit-row stride must be a multiple of 4 "
+               "words covering d_out");
+  GCNB_REQUIRE(dense_tc_applies(d_in, d_out), "dense bits: widths %d -> %d have no tcgen05 engine", d_in, d_out);
+  if (n_rows == 0) return GCNB_OK;
+  return launch_dense_tc(x, ldx, nullptr, n_rows, d_in, w, d_out, y, ldy, GCNB_ACT_RELU, (cudaStream_t)stream,
+                         nullptr, 0, nullptr, 0, nullptr, 0, bits, ld_bits);
+}
+
 extern "C" int gcnb_bwd_grid(int32_t n_rows, int32_t d_prev, int32_t d_k, int32_t with_gprev, int32_t* grid_out) {
   GCNB_REQUIRE(grid_out != nullptr, "bwd grid: null output");
   GCNB_REQUIRE(d_prev >= 1 && d_prev <= 256 && d_k >= 1 && d_k <= 256, "bwd grid: widths out of range");
@@ -927,8 +951,10 @@ extern "C" int gcnb_dw_f32(const float* x, int32_t ldx, int32_t d_prev, const fl
 
 extern "C" int gcnb_bwd_epilogue_f32(const float* agg, int32_t ldagg, int32_t d_k, const float* h_prev,
                                      int32_t ldhp, int32_t d_prev, const float* w, float* g_prev, int32_t ldgp,
-                                     int32_t act, const int32_t* rows, int32_t n_rows, float* dw_partials,
-                                     void* stream) {
+                                     int32_t act, const uint32_t* hbits, int32_t ld_hbits, const int32_t* rows,
+                                     int32_t n_rows, float* dw_partials, void* stream) {
+  GCNB_REQUIRE(!hbits || (ld_hbits % 4 == 0 && ld_hbits * 32 >= d_prev && aligned16(hbits)),
+               "bwd epilogue: sign-bit rows need a stride of >= d_prev/32 words, a multiple of 4");
   GCNB_REQUIRE(n_rows >= 0, "bwd epilogue: n_rows must be >= 0");
   GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "bwd epilogue: unknown activation %d", act);
   GCNB_REQUIRE(d_prev >= 1 && d_prev <= 256 && d_k >= 1 && d_k <= 256, "bwd epilogue: widths out of range");
@@ -942,7 +968,7 @@ extern "C" int gcnb_bwd_epilogue_f32(const float* agg, int32_t ldagg, int32_t d_
   if (int rc = bwd_plan(n_rows, d_prev, d_k, g_prev != nullptr, &plan)) return rc;
   if (n_rows == 0) return GCNB_OK;
   return launch_bwd_epilogue(agg, ldagg, d_k, h_prev, ldhp, d_prev, w, g_prev, ldgp, act, rows, n_rows, dw_partials,
-                             plan, (cudaStream_t)stream);
+                             plan, (cudaStream_t)stream, hbits, ld_hbits);
 }
 
 extern "C" int gcnb_bwd_workspace_ld(int32_t d_prev, int32_t d_k, int32_t* ld_out) {

@@ -294,6 +294,14 @@ class ProcState:
                     self.fwd_ws[k] = torch.zeros((max(n, 1), devmem.ld_of(self.dims[k - 1])), dtype=torch.float32,
                                                  device=dev)
             self.dw1_from_fwd = bool(reuse_fwd_aggregate and L >= 1 and self.fwd_ws[1] is not None)
+            # sign bits of H^k (σ' of a ReLU layer) written by the split forward's
+            # tcgen05 transform, read by the next layer's backward mask (1/32 of H's bytes)
+            self.hbits = [None] * (L + 1)
+            self.hbits_valid = [False] * (L + 1)
+            for k in range(1, L):
+                if not self.transform_first[k] and self.fwd_ws[k] is not None and self.activation == "relu":
+                    words = -(-self.dims[k] // 32)
+                    self.hbits[k] = torch.zeros((max(n, 1), -(-words // 4) * 4), dtype=torch.int32, device=dev)
             # split-mode workspace (agg rows) for large-ΔW layers (gcnb_bwd_workspace_ld)
             self.bwd_ws = [None] * (L + 1)
             for k in range(1, L + 1):
@@ -456,9 +464,15 @@ class ProcState:
             return
         ws, h = self.fwd_ws[k], self.hbuf[k]
         n, width, d_out = self.n_own, self.dims[k - 1], self.dims[k]
+        bits = self.hbits[k]
+        self.hbits_valid[k] = bits is not None and _lib.dense_tc_applies(width, d_out)
         with span(f"dense{k}", 4 * (n * width + width * d_out + n * d_out), 2 * n * width * d_out, self.stream()):
-            _lib.call("gcnb_dense_f32", ws.data_ptr(), ws.shape[1], None, n, width, self.w[k].data_ptr(), d_out,
-                      h.data_ptr(), h.shape[1], self.act, self.stream())
+            if self.hbits_valid[k]:
+                _lib.call("gcnb_dense_bits_f32", ws.data_ptr(), ws.shape[1], n, width, self.w[k].data_ptr(), d_out,
+                          h.data_ptr(), h.shape[1], bits.data_ptr(), bits.shape[1], self.stream())
+            else:
+                _lib.call("gcnb_dense_f32", ws.data_ptr(), ws.shape[1], None, n, width, self.w[k].data_ptr(), d_out,
+                          h.data_ptr(), h.shape[1], self.act, self.stream())
 
     def bwd_split(self, k: int) -> bool:
         """Layer k's backward runs as aggregation + dense epilogue (bwd_finish)."""
@@ -475,11 +489,14 @@ class ProcState:
         used = self.bwd_grids[k][2]
         if n == 0:
             return 0
-        algo = 4 * n * (dk + 2 * dp) + 4 * dp * dk * used + (4 * dp * n if gp is not None else 0)
-        with span(f"bwd{k}", algo, 2 * n * dp * dk * (2 if gp is not None else 1), self.stream()):
+        bits = self.hbits[k - 1] if gp is not None and self.hbits_valid[k - 1] else None
+        mask_bytes = (4 * n * bits.shape[1] if bits is not None else 4 * dp * n) if gp is not None else 0
+        algo = 4 * n * (dk + dp) + 4 * dp * dk * used + mask_bytes + (4 * dp * n if gp is not None else 0)
+        with span(f"bwd{k}_dense", algo, 2 * n * dp * dk * (2 if gp is not None else 1), self.stream()):
             _lib.call("gcnb_bwd_epilogue_f32", ws.data_ptr(), ws.shape[1], dk, hp.data_ptr(), hp.shape[1], dp,
                       self.w[k].data_ptr(), 0 if gp is None else gp.data_ptr(), 0 if gp is None else gp.shape[1],
-                      self.act, None, n, self.partials[k].data_ptr(), self.stream())
+                      self.act, None if bits is None else bits.data_ptr(), 0 if bits is None else bits.shape[1],
+                      None, n, self.partials[k].data_ptr(), self.stream())
         return used
 
     def loss_grad(self, inv_n_labeled: float) -> None:
@@ -499,8 +516,10 @@ class ProcState:
         gi, gb, ga = self.bwd_grids[k]
         used = {"all": ga, "interior": gi, "boundary": gb}[rows]
         g = self.gext[k]
-        if rows != "all" and self.bwd_split(k):
-            # row list of an overlapped exchange: aggregate only (bwd_finish does the rest)
+        if self.bwd_split(k):
+            # aggregation alone (span bwd{k}); the dense epilogue (G^{k-1}, ΔW^k
+            # partials) runs over all own rows in bwd_finish — right away for
+            # rows="all", after the boundary rows for an overlapped exchange
             op_nnz = op.nnz_of(rows)
             ws = self.bwd_ws[k]
             with span(f"bwd{k}", 4 * (n_sel + 1) + 8 * op_nnz + 4 * self.dims[k] * (op_nnz + n_sel), 2 * op_nnz *
@@ -508,7 +527,7 @@ class ProcState:
                 _lib.call("gcnb_spmm_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(), op.csr.val.data_ptr(),
                           sel, n_sel, g.data_ptr(), g.shape[1], self.dims[k], ws.data_ptr(), ws.shape[1],
                           self.stream())
-            return 0
+            return self.bwd_finish(k) if rows == "all" else 0
         hp = self.hbuf[k - 1]
         gp = self.gext[k - 1] if k > 1 else None
         part = self.partials[k][slot:]
@@ -540,7 +559,7 @@ class ProcState:
         used = self.bwd_grids[1][2]
         if n == 0:
             return 0
-        with span("bwd1", 4 * n * (dp + dk) + 4 * dp * dk * used, 2 * n * dp * dk, self.stream()):
+        with span("bwd1_dense", 4 * n * (dp + dk) + 4 * dp * dk * used, 2 * n * dp * dk, self.stream()):
             _lib.call("gcnb_dw_f32", x.data_ptr(), x.shape[1], dp, g.data_ptr(), g.shape[1], dk, None, n,
                       self.partials[1].data_ptr(), self.stream())
         return used

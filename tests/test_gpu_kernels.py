@@ -397,3 +397,40 @@ def test_sum_buffers_rank_order_and_sgd():
     w0 = w.clone()
     _lib.call("gcnb_sgd_f32", w.data_ptr(), out.data_ptr(), 1000, 0.1, devmem.stream_handle(None, dv))
     assert torch.allclose(w, w0 - 0.1 * out, rtol=0, atol=1e-6)
+
+
+def test_dense_sign_bits_and_bit_masked_epilogue():
+    """gcnb_dense_bits_f32 writes H = relu(X·W) and its sign bits (bit m of word
+    m/32 = H[m] > 0); the backward epilogue masked by those bits gives exactly the
+    G_prev and ΔW of the fp32-masked epilogue."""
+    n, d_in, d_h, d_k = 128 * 148 * 2 + 45, 100, 128, 47
+    rng = np.random.default_rng(31)
+    x = rng.standard_normal((n, d_in))
+    w1 = rng.uniform(-0.2, 0.2, (d_in, d_h))
+    d = dev()
+    xd, w1d = devmem.upload_dense(x, d), devmem.upload_dense(w1, d)
+    hd = devmem.empty_rows(n, d_h, d)
+    bits = torch.zeros((n, 4), dtype=torch.int32, device=d)
+    st = devmem.stream_handle(None, d)
+    _lib.call("gcnb_dense_bits_f32", xd.data_ptr(), xd.shape[1], n, d_in, w1d.data_ptr(), d_h, hd.data_ptr(),
+              hd.shape[1], bits.data_ptr(), 4, st)
+    h = devmem.download(hd, n, d_h)
+    close(h, np.maximum(o.dmm(x, w1), 0))
+    b = bits.cpu().numpy().view(np.uint32)
+    got = ((b[:, np.arange(d_h) // 32] >> (np.arange(d_h) % 32)) & 1).astype(bool)
+    assert np.array_equal(got, h > 0)
+    # backward epilogue from a resident aggregate: float mask vs bit mask
+    agg = rng.standard_normal((n, d_k))
+    w2 = rng.uniform(-0.2, 0.2, (d_h, d_k))
+    aggd, w2d = devmem.upload_dense(agg, d, ld=_lib.bwd_workspace_ld(d_h, d_k)), devmem.upload_dense(w2, d)
+    grid = _lib.bwd_grid(n, d_h, d_k, True)
+    outs = []
+    for use_bits in (False, True):
+        gpd = devmem.empty_rows(n, d_h, d)
+        part = torch.zeros((grid, d_h * devmem.ld_of(d_k)), dtype=torch.float32, device=d)
+        _lib.call("gcnb_bwd_epilogue_f32", aggd.data_ptr(), aggd.shape[1], d_k, hd.data_ptr(), hd.shape[1], d_h,
+                  w2d.data_ptr(), gpd.data_ptr(), gpd.shape[1], _lib.ACT["relu"],
+                  bits.data_ptr() if use_bits else None, 4 if use_bits else 0, None, n, part.data_ptr(), st)
+        outs.append((devmem.download(gpd, n, d_h), part.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    close(outs[1][0], o.dmm(agg, w2.T.copy()) * (h > 0))
