@@ -132,15 +132,15 @@ int g_dense_mode = 0;  // 0 auto, 1 force SIMT, 2 force tensor core (where it ap
 //   warps 0-7   epilogue: tcgen05.ld → act / ⊙σ'(mask) → coalesced stores
 //               (two warps per TMEM lane quarter, each half of the tile's rows);
 //               warps 0-3 also write Wᵀ hi/lo into TMEM at start
-//   warps 8-11  producer: cp.async X (and mask) tile → stage
-//   warps 12-15 converter: lo(x) in place once the stage's hi MMAs drained
-//   warp 16     TMEM owner; lane 0 issues the MMAs, software-pipelined as
+//   warps 8-11  converter: lo(x) in place once the stage's hi MMAs drained
+//   warps 12-14 producer: cp.async X (and mask) tile → stage (TMA: one thread)
+//   warp 15     TMEM owner; lane 0 issues the MMAs, software-pipelined as
 //               hi(t) · lo(t-1) so the tensor core runs while tile t converts
 // Accumulators: two buffers of NT_ columns at TMEM column 256.
-constexpr int DT_WARPS = 17;
+constexpr int DT_WARPS = 16;  // 4 per SM sub-partition: up to 128 registers per thread
 constexpr int DT_THREADS = DT_WARPS * 32;
-constexpr int DT_PROD = 128;  // producer threads (warps 8-11)
-constexpr int DT_CONV = 128;  // converter threads (warps 12-15)
+constexpr int DT_PROD = 96;   // producer threads (warps 12-14)
+constexpr int DT_CONV = 128;  // converter threads (warps 8-11)
 constexpr int DT_EPI = 256;   // epilogue threads (warps 0-7)
 constexpr int DT_MAX_STAGES = 4;
 
@@ -204,7 +204,7 @@ __device__ __forceinline__ void load_mask_rows(uint32_t stage, const float* __re
 
 }  // namespace
 
-// TMA (rows == nullptr): one thread of warp 8 streams each tile with Kb/32
+// TMA (rows == nullptr): one thread of warp 12 streams each tile with Kb/32
 // SWIZZLE_128B boxes of 32 floats × NT_ rows (out-of-range K and rows arrive
 // as zeros) plus, masked, one box of the mask rows; completion is counted by
 // the stage's mbarrier (expect_tx), so loads run up to S tiles ahead.
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
     const int r = rem % NT_, c = kc + rem / NT_;
     *reinterpret_cast<float4*>(smem + sidx * st_bytes + sw128_off(r, c, NT_)) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  if (warp == 16) {
+  if (warp == 15) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(&tmem_base_slot))
                  : "memory");
@@ -295,9 +295,9 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
   __syncthreads();
   tc_after_sync();
 
-  if (TMA && warp >= 8 && warp < 12) {
+  if (TMA && warp >= 12 && warp < 15) {
     // ---------------- producer (TMA)
-    if (warp == 8 && lane == 0) {
+    if (warp == 12 && lane == 0) {
       const uint32_t tx = (uint32_t)(Kb / 32) * NT_ * 128 + m_bytes;
       int t = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
@@ -310,9 +310,9 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= 8 && warp < 12) {
+  } else if (warp >= 12 && warp < 15) {
     // ---------------- producer (cp.async, row list)
-    const int tid = threadIdx.x - 256;
+    const int tid = threadIdx.x - 384;
     int t = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
       const int s = t % S;
@@ -332,9 +332,9 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
       fence_async_smem();
       mbar_arrive(bar(0, (t - 1) % S));
     }
-  } else if (warp >= 12 && warp < 16) {
+  } else if (warp >= 8 && warp < 12) {
     // ---------------- lo(x) converter
-    const int tid = threadIdx.x - 384;
+    const int tid = threadIdx.x - 256;
     int t = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
       const int s = t % S;
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
       fence_async_smem();
       mbar_arrive(bar(2, s));
     }
-  } else if (warp == 16) {
+  } else if (warp == 15) {
     // ---------------- MMA issuer: hi(t) then lo(t-1)
     if (lane == 0) {
       const uint32_t idesc = idesc_tf32(128, NT_);
@@ -403,19 +403,33 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
       const float* ms = reinterpret_cast<const float*>(smem + s * st_bytes + x_bytes);
       const uint32_t* mw = reinterpret_cast<const uint32_t*>(ms);
       const int i0 = tile * NT_;
-      for (int n0 = hs * span; n0 < (hs + 1) * span && i0 + n0 < n_rows; n0 += 16) {
-        uint32_t v[16];
-        const uint32_t taddr = acc0 + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NT_ + n0);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      // drain this warp's half of the accumulator into registers first and
+      // release it, so the MMAs of tile t+2 overlap the stores of tile t
+      const int ng = span / 16;
+      uint32_t v[4][16];
+#pragma unroll
+      for (int gi = 0; gi < 4; ++gi) {
+        if (gi < ng) {
+          const uint32_t taddr = acc0 + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NT_ + hs * span + 16 * gi);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[gi][0]), "=r"(v[gi][1]), "=r"(v[gi][2]), "=r"(v[gi][3]), "=r"(v[gi][4]), "=r"(v[gi][5]),
+                "=r"(v[gi][6]), "=r"(v[gi][7]), "=r"(v[gi][8]), "=r"(v[gi][9]), "=r"(v[gi][10]), "=r"(v[gi][11]),
+                "=r"(v[gi][12]), "=r"(v[gi][13]), "=r"(v[gi][14]), "=r"(v[gi][15])
+              : "r"(taddr));
+        }
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tc_before_sync();
+      mbar_arrive(abar(1, b));
+#pragma unroll
+      for (int gi = 0; gi < 4; ++gi) {
+        const int n0 = hs * span + 16 * gi;
+        if (gi >= ng || i0 + n0 >= n_rows) continue;
         float o[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          o[j] = __uint_as_float(v[j]);
+          o[j] = __uint_as_float(v[gi][j]);
           if (MK == 1) {
             const float hv = m_mask ? ms[(n0 + j) * mpad + m] : 1.0f;
             o[j] = RELU ? (hv > 0.0f ? o[j] : 0.0f) : o[j];
@@ -450,15 +464,13 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
           }
         }
       }
-      tc_before_sync();
-      mbar_arrive(abar(1, b));
       if (MASKED) mbar_arrive(bar(3, s));
     }
   }
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
-  if (warp == 16) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  if (warp == 15) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
 namespace {
