@@ -651,6 +651,18 @@ int tile_rows(int d_out, int lpr, int* rpt_out) {
 
 using AggFn = void (*)(const int*, const int*, const float*, const int*, int, const float4*, int, int, float4*, int,
                        int, int*, int);
+// Shape of the aggregation-only kernel: two float4 chunks per lane from 9 chunks
+// up, so 2-4 rows share a warp (rows of similar length side by side after the
+// degree-sorted layout windows): measured on the products shape, d=104 took
+// 3.43 ms as (16,2) vs 3.59 ms as (32,1), d=48 1.82 ms as (8,2) vs 1.86 ms as (16,1)
+// (profiles/r01_spmm_shapes_products.txt).
+AggShape agg_shape_spmm(int d) {
+  const int c4 = round4(d) / 4;
+  if (c4 > 8 && c4 <= 16) return {8, 2};
+  if (c4 > 16 && c4 <= 32) return {16, 2};
+  return agg_shape(d);
+}
+
 #define GCNB_AGG_EXTRA_CASES(M) M(4, 3) M(8, 2) M(8, 4) M(16, 2)
 AggFn pick_agg(AggShape s) {
 #define M(L, V) if (s.lpr == L && s.vpl == V) return k_agg<L, V>;
@@ -756,7 +768,7 @@ int check_csr_args(const int32_t* row_ptr, const int32_t* col, const float* val,
 int launch_agg(const int32_t* row_ptr, const int32_t* col, const float* val, const int32_t* rows, int32_t n_rows,
                const float* x, int32_t ldx, int32_t d, float* y, int32_t ldy, int32_t act, cudaStream_t st,
                const char* what) {
-  AggShape s = agg_shape(d);
+  AggShape s = agg_shape_spmm(d);
   if (g_agg_lpr > 0 && g_agg_lpr * g_agg_vpl * 4 >= round4(d)) s = {g_agg_lpr, g_agg_vpl};
   AggFn fn = pick_agg(s);
   GCNB_REQUIRE(fn != nullptr, "%s: no aggregation kernel for lpr=%d vpl=%d", what, s.lpr, s.vpl);
