@@ -651,11 +651,12 @@ int tile_rows(int d_out, int lpr, int* rpt_out) {
 
 using AggFn = void (*)(const int*, const int*, const float*, const int*, int, const float4*, int, int, float4*, int,
                        int, int*, int);
-// Shape of the aggregation-only kernel: two float4 chunks per lane from 9 chunks
-// up, so 2-4 rows share a warp (rows of similar length side by side after the
-// degree-sorted layout windows): measured on the products shape, d=104 took
-// 3.43 ms as (16,2) vs 3.59 ms as (32,1), d=48 1.82 ms as (8,2) vs 1.86 ms as (16,1)
-// (profiles/r01_spmm_shapes_products.txt).
+// Shape of the aggregation-only kernel over all own rows: two float4 chunks per
+// lane from 9 chunks up, so 2-4 rows share a warp (rows of similar length side by
+// side after the degree-sorted layout windows): measured on the products shape,
+// d=104 took 3.43 ms as (16,2) vs 3.59 ms as (32,1), d=48 1.82 ms as (8,2) vs
+// 1.86 ms as (16,1) (profiles/r01_spmm_shapes_products.txt).  On the interior /
+// boundary row lists of 2-4 GPU runs the same shapes were 10-25 % slower.
 AggShape agg_shape_spmm(int d) {
   const int c4 = round4(d) / 4;
   if (c4 > 8 && c4 <= 16) return {8, 2};
@@ -768,7 +769,9 @@ int check_csr_args(const int32_t* row_ptr, const int32_t* col, const float* val,
 int launch_agg(const int32_t* row_ptr, const int32_t* col, const float* val, const int32_t* rows, int32_t n_rows,
                const float* x, int32_t ldx, int32_t d, float* y, int32_t ldy, int32_t act, cudaStream_t st,
                const char* what) {
-  AggShape s = agg_shape_spmm(d);
+  // row lists (interior / boundary rows of an overlapped exchange) keep one row
+  // group per 16-32 lanes: pairing rows of a list measured slower at 2-4 GPUs
+  AggShape s = rows ? agg_shape(d) : agg_shape_spmm(d);
   if (g_agg_lpr > 0 && g_agg_lpr * g_agg_vpl * 4 >= round4(d)) s = {g_agg_lpr, g_agg_vpl};
   AggFn fn = pick_agg(s);
   GCNB_REQUIRE(fn != nullptr, "%s: no aggregation kernel for lpr=%d vpl=%d", what, s.lpr, s.vpl);
