@@ -144,7 +144,8 @@ int gcnb_dense_bits_f32(const float* x, int32_t ldx, int32_t n_rows, int32_t d_i
  * the aggregation kernel for every width it covers (0, 0 = automatic). */
 int gcnb_set_agg_shape(int32_t lpr, int32_t vpl);
 /* Test/tuning knob: gathers of the aggregation kernel staged through shared
- * memory with cp.async (0, default) or batched in registers (1). */
+ * memory with cp.async.cg (0, default), batched in registers (1), or staged
+ * with L1-allocating cp.async.ca (2). */
 int gcnb_set_agg_gather(int32_t mode);
 
 /* runtime._bwd_compute (runtime.py:344-356) for the row list `rows`:

@@ -100,6 +100,8 @@ def load() -> ctypes.CDLL:
         fn.restype = res
         fn.argtypes = args
     _lib = lib
+    if os.environ.get("GCNB_AGG_GATHER"):  # tuning knob (gcnb_set_agg_gather), e.g. for A/B bench runs
+        check(lib.gcnb_set_agg_gather(int(os.environ["GCNB_AGG_GATHER"])))
     return lib
 
 

@@ -113,15 +113,24 @@ __device__ __forceinline__ void aggregate_span(const int* __restrict__ col, cons
 // its sector request through L1/L2 (ncu measured 1.5x the algorithmic gather
 // bytes on products from the idle chunk lanes), a predicated one does not.
 // The slot then holds stale data, so callers must not consume it.
+// CA: allocate the gathered sectors in L1 as well (cp.async.ca) so warps of one
+// SM that share neighbours (locality layout) hit L1 instead of the L2 fabric.
+template <bool CA = false>
 __device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src, bool pred) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
-      "@q cp.async.cg.shared.global [%0], [%1], 16;\n\t}" ::"r"(s), "l"(gmem_src), "r"((int)pred)
-      : "memory");
+  if constexpr (CA)
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+        "@q cp.async.ca.shared.global [%0], [%1], 16;\n\t}" ::"r"(s), "l"(gmem_src), "r"((int)pred)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+        "@q cp.async.cg.shared.global [%0], [%1], 16;\n\t}" ::"r"(s), "l"(gmem_src), "r"((int)pred)
+        : "memory");
 }
 
-template <int LPR, int VPL, int U>
+template <int LPR, int VPL, int U, bool CA = false>
 __device__ __forceinline__ void aggregate_span_cp(const int* __restrict__ col, const float* __restrict__ val, int s,
                                                   int len, const float4* __restrict__ X4, int ldx4, int c4, int gl,
                                                   float4 (&acc)[VPL], float4* __restrict__ stage) {
@@ -155,7 +164,7 @@ __device__ __forceinline__ void aggregate_span_cp(const int* __restrict__ col, c
 #pragma unroll
         for (int q = 0; q < VPL; ++q) {
           const int ch = gl + q * LPR;
-          cp_async_16(stage + (u * VPL + q) * 32 + lane, xr + ch, okv[u] && ch < c4);
+          cp_async_16<CA>(stage + (u * VPL + q) * 32 + lane, xr + ch, okv[u] && ch < c4);
         }
       }
       asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
@@ -247,7 +256,8 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
     float4 acc[VPL];
 #pragma unroll
     for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (regs) aggregate_span<LPR, VPL>(col, val, s, len, X4, ldx4, c4, gl, acc);
+    if (regs == 1) aggregate_span<LPR, VPL>(col, val, s, len, X4, ldx4, c4, gl, acc);
+    else if (regs == 2) aggregate_span_cp<LPR, VPL, U, true>(col, val, s, len, X4, ldx4, c4, gl, acc, stage);
     else aggregate_span_cp<LPR, VPL, U>(col, val, s, len, X4, ldx4, c4, gl, acc, stage);
     if (row >= 0) {
 #pragma unroll
@@ -613,7 +623,7 @@ struct AggShape {
 
 // Forced (lpr, vpl) for the aggregation-only kernel (gcnb_set_agg_shape; 0 = auto).
 int g_agg_lpr = 0, g_agg_vpl = 0;
-int g_agg_regs = 0;  // 1: register-batched gathers instead of cp.async staging (gcnb_set_agg_gather)
+int g_agg_regs = 0;  // 1: register-batched gathers, 2: L1-allocating cp.async.ca staging (gcnb_set_agg_gather)
 
 AggShape agg_shape(int d) {
   const int c4 = round4(d) / 4;
@@ -826,7 +836,8 @@ extern "C" int gcnb_set_agg_shape(int32_t lpr, int32_t vpl) {
 }
 
 extern "C" int gcnb_set_agg_gather(int32_t mode) {
-  GCNB_REQUIRE(mode == 0 || mode == 1, "agg gather mode: 0 (cp.async staging) or 1 (register batches)");
+  GCNB_REQUIRE(mode >= 0 && mode <= 2,
+               "agg gather mode: 0 (cp.async.cg staging), 1 (register batches), 2 (cp.async.ca staging)");
   g_agg_regs = mode;
   return GCNB_OK;
 }
