@@ -119,9 +119,13 @@ __global__ void __launch_bounds__(NT) k_loss(const float4* __restrict__ H4, int 
   const float inv = (float)inv_n;
   double local = 0.0;
   const int warp_global = blockIdx.x * WARPS + warp;
-  for (int row0 = warp_global * GPW; row0 < n_rows; row0 += gridDim.x * WARPS * GPW) {
+  const int stride = gridDim.x * WARPS * GPW;
+  // the next row's label is fetched one iteration ahead (hides its latency)
+  int y_next = warp_global * GPW + gw < n_rows ? __ldg(label + warp_global * GPW + gw) : -1;
+  for (int row0 = warp_global * GPW; row0 < n_rows; row0 += stride) {
     const int row = row0 + gw;
-    const int y = row < n_rows ? __ldg(label + row) : -1;
+    const int y = y_next;
+    y_next = row + stride < n_rows ? __ldg(label + row + stride) : -1;
     float4 hv[VPL];
     float m = -INFINITY;
 #pragma unroll
