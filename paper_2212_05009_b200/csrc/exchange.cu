@@ -126,6 +126,11 @@ __global__ void __launch_bounds__(NT) k_loss(const float4* __restrict__ H4, int 
     const int row = row0 + gw;
     const int y = y_next;
     y_next = row + stride < n_rows ? __ldg(label + row + stride) : -1;
+    if (!__any_sync(0xffffffffu, y >= 0)) {  // no labelled row in this warp (warp-uniform): zeros only
+      if (row < n_rows)
+        for (int ch = gl; ch < ldg4; ch += LPR) G4[(size_t)row * ldg4 + ch] = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
     float4 hv[VPL];
     float m = -INFINITY;
 #pragma unroll
