@@ -373,17 +373,38 @@ def run_single(args):
     h0_host = np.zeros(tuple(hb.shape), dtype=np.float32)
     h0_host[:, :d0] = wl["h0"][states[0].global_rows]
     h0_pinned = torch.from_numpy(h0_host).pin_memory()
-    e2e_times = []
+    # Input pipeline (a data loader's prefetch): step i+1's features are uploaded
+    # on a copy stream into a device staging buffer while step i trains; each
+    # step starts with a device-to-device move staging -> features.  Every
+    # step's H2D is inside the one timed region (the first one is not hidden).
     m = [None]
-    for i in range(0 if args.kernels_only else max(3, min(args.steps, 20))):
-        flush.zero_()
+    e2e_steps = 0 if args.kernels_only else max(3, min(args.steps, 20))
+    e2e_ms = float("nan")
+    if e2e_steps:
+        stage = torch.empty_like(hb)
+        cur = torch.cuda.current_stream(dev)
+        up = torch.cuda.Stream(dev)
+
+        def upload():
+            up.wait_stream(cur)  # the staging buffer has been consumed
+            with torch.cuda.stream(up):
+                stage.copy_(h0_pinned, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(up)
+            return ev
+
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        hb.copy_(h0_pinned, non_blocking=True)
-        m = gb.train_epochs(states, net, wl["labels"], 1)
+        up_done = upload()
+        for i in range(e2e_steps):
+            flush.zero_()
+            cur.wait_event(up_done)
+            hb.copy_(stage)
+            if i + 1 < e2e_steps:
+                up_done = upload()
+            m = gb.train_epochs(states, net, wl["labels"], 1)  # ends with the loss D2H
         torch.cuda.synchronize()
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_ms = 1e3 * float(np.mean(e2e_times)) if e2e_times else float("nan")
+        e2e_ms = 1e3 * (time.perf_counter() - t0) / e2e_steps
     h2d = int(h0_pinned.numel() * 4)  # features (the label map stays resident: same LabelSet)
     d2h = 8 * 1  # the epoch loss
 
@@ -403,7 +424,8 @@ def run_single(args):
                    "reuse_fwd_aggregate": states[0].dw1_from_fwd,
                    "graph": not args.no_graph, "seed": args.seed},
         "e2e": {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "loss_last": m[0].loss if m[0] is not None else None},
+                "loss_last": m[0].loss if m[0] is not None else None,
+                "input_pipeline": "step i+1's H2D (copy stream, pinned) overlaps step i; D2D staging->features per step"},
         "gpu_launches": int(launches_per_epoch * args.steps),
         "roofline": roofline_line(kname, achieved, peak, peak_kind, traffic_for(wl["name"], kname), kbytes, kms),
         "kernels": table,
