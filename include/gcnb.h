@@ -49,6 +49,9 @@ enum { GCNB_ACT_RELU = 0, GCNB_ACT_IDENTITY = 1 };
 /* ---- library / diagnostics ------------------------------------------- */
 const char* gcnb_last_error(void);
 int gcnb_version(void);
+/* mbarrier-pipeline watchdog (dense_tc / aggwin): trap after `ms` of a stuck
+ * wait; default 60000, 0 = never (env GCNB_WATCHDOG_MS at load). */
+int gcnb_set_watchdog_ms(int64_t ms);
 /* number of kernels this library has launched in this process (all threads) */
 uint64_t gcnb_launch_count(void);
 int gcnb_device_count(int* out);
@@ -81,6 +84,23 @@ int gcnb_spmm_f32(const int32_t* row_ptr, const int32_t* col, const float* val,
                   const int32_t* rows, int32_t n_rows,
                   const float* x, int32_t ldx, int32_t d,
                   float* y, int32_t ldy, void* stream);
+
+/* Windowed form of gcnb_spmm_f32 for ALL own rows (rows == NULL), the SpMM of
+ * runtime._fwd_compute / _bwd_compute (runtime.py:299, 346) over a whole row
+ * block.  gcnb_window_csr re-orders each row's nonzeros near-first into int2
+ * entries {ring slot | column, value bits} (entries: nnz int2, nnear: n_rows
+ * int32) — once per operator, `bt` = window half-width in 128-row tiles, n_own =
+ * own rows (halo columns are never near).  gcnb_aggwin_f32 then computes
+ * Y[r] = act(Σ A[r,j]·X[j]) with the window rows staged in shared memory by TMA
+ * (X rows 0..n_rows-1 are the own rows; far columns may index halo rows).
+ * Summation order: near entries then far entries, each in CSR order (fixed).
+ * act: GCNB_ACT_RELU / GCNB_ACT_IDENTITY, or -1 for a plain store. */
+int gcnb_window_csr(const int32_t* row_ptr, const int32_t* col, const float* val, int32_t n_rows,
+                    int32_t n_own, int32_t bt, int32_t* nnear, void* entries, void* stream);
+int gcnb_aggwin_applies(int32_t d, int32_t bt, int32_t* out);
+int gcnb_aggwin_f32(const int32_t* row_ptr, const int32_t* nnear, const void* entries, int32_t n_rows,
+                    int32_t bt, const float* x, int32_t ldx, int32_t d, float* y, int32_t ldy, int32_t act,
+                    void* stream);
 
 /* sparse.gather_rows (sparse.py:237-261) and the send-side pack of
  * runtime._fwd_send/_bwd_send (runtime.py:289-294, 336-341), fused with the

@@ -28,6 +28,7 @@ _f64 = ctypes.c_double
 _SIGNATURES = {
     "gcnb_last_error": (ctypes.c_char_p, []),
     "gcnb_version": (_c_int, []),
+    "gcnb_set_watchdog_ms": (_c_int, [_c_i64]),
     "gcnb_launch_count": (ctypes.c_uint64, []),
     "gcnb_device_count": (_c_int, [ctypes.POINTER(_c_int)]),
     "gcnb_malloc": (_c_int, [ctypes.POINTER(_vp), ctypes.c_size_t]),
@@ -43,6 +44,9 @@ _SIGNATURES = {
     "gcnb_event_elapsed_ms": (_c_int, [_vp, _vp, ctypes.POINTER(_f32)]),
     "gcnb_stream_is_capturing": (_c_int, [_vp, ctypes.POINTER(_c_int)]),
     "gcnb_spmm_f32": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp]),
+    "gcnb_window_csr": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
+    "gcnb_aggwin_applies": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_int)]),
+    "gcnb_aggwin_f32": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp]),
     "gcnb_pack_rows_f32": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _vp, _c_int, _vp, _vp, _vp]),
     "gcnb_wait_flags": (_c_int, [_vp, _vp, _c_int, _vp, _vp, _c_int, _vp]),
     "gcnb_fwd_layer_f32": (
@@ -100,6 +104,8 @@ def load() -> ctypes.CDLL:
         fn.restype = res
         fn.argtypes = args
     _lib = lib
+    if os.environ.get("GCNB_WATCHDOG_MS"):
+        check(lib.gcnb_set_watchdog_ms(int(os.environ["GCNB_WATCHDOG_MS"])))
     if os.environ.get("GCNB_AGG_GATHER"):  # tuning knob (gcnb_set_agg_gather), e.g. for A/B bench runs
         check(lib.gcnb_set_agg_gather(int(os.environ["GCNB_AGG_GATHER"])))
     return lib
@@ -161,6 +167,12 @@ def bwd_workspace_ld(d_prev: int, d_k: int) -> int:
     out = ctypes.c_int32(0)
     call("gcnb_bwd_workspace_ld", d_prev, d_k, ctypes.byref(out))
     return int(out.value)
+
+
+def aggwin_applies(d: int, bt: int) -> bool:
+    out = _c_int(0)
+    call("gcnb_aggwin_applies", d, bt, ctypes.byref(out))
+    return bool(out.value)
 
 
 def loss_scratch_doubles() -> int:

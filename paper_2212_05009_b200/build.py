@@ -2,11 +2,15 @@
 
 The library is compiled straight from `csrc/*.cu` (no torch extension
 machinery, no JIT cache) so the built .so travels with the repo snapshot to
-the GPU box.  Rebuilds only when a source or header is newer than the .so.
+the GPU box.  Rebuilds when the content hash of the sources, headers and
+flags differs from the one recorded next to the .so (lib/BUILD_HASH), so a
+shipped binary is provably built from the tree it travels with
+(`build_hash()` is reported in every bench line).
 """
 
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -37,28 +41,49 @@ def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
 
+HASH_FILE = LIB_DIR / "BUILD_HASH"
+
+
+def source_hash() -> str:
+    """sha256 over every source, header and the compile flags (first 16 hex digits)."""
+    h = hashlib.sha256()
+    for p in sources() + sorted(CSRC.glob("*.cuh")) + HEADERS:
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    h.update(" ".join(NVCC_FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
+def build_hash() -> str | None:
+    """Hash recorded when lib/libgcnb.so was built (None if unknown)."""
+    return HASH_FILE.read_text().strip() if HASH_FILE.exists() and LIB.exists() else None
+
+
 def needs_build() -> bool:
-    if not LIB.exists():
-        return True
-    t = LIB.stat().st_mtime
-    deps = sources() + sorted(CSRC.glob("*.cuh")) + HEADERS + [Path(__file__)]
-    return any(p.stat().st_mtime > t for p in deps)
+    return not LIB.exists() or build_hash() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
+    digest = source_hash()
     objs = []
     log = []
-    for src in sources():
+    procs = []
+    for src in sources():  # one nvcc per translation unit, in parallel
         obj = LIB_DIR / (src.stem + ".o")
         cmd = [nvcc(), *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {src.name}:\n{r.stdout}\n{r.stderr}")
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(str(obj))
+    failed = []
+    for src, pr in procs:
+        out, _ = pr.communicate()
+        log.append(out)
+        if pr.returncode != 0:
+            failed.append(f"nvcc failed on {src.name}:\n{out}")
+    if failed:
+        raise RuntimeError("\n".join(failed))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(tmp), *objs,
            "-lcudart"]
@@ -66,6 +91,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    HASH_FILE.write_text(digest + "\n")
     (LIB_DIR / "ptxas.log").write_text("\n".join(log))
     if verbose:
         print("\n".join(log))

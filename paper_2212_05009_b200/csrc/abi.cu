@@ -5,6 +5,7 @@
 #include <map>
 #include <mutex>
 #include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -92,7 +93,23 @@ using namespace gcnb;
 
 extern "C" const char* gcnb_last_error(void) { return t_err; }
 
-extern "C" int gcnb_version(void) { return 100; }  // 0.1.0
+namespace gcnb {
+// Host setters of every translation unit's watchdog limit (sync.cuh).
+static std::vector<int (*)(unsigned long long)>& watchdog_setters() {
+  static std::vector<int (*)(unsigned long long)> v;
+  return v;
+}
+void register_watchdog_setter(int (*fn)(unsigned long long)) { watchdog_setters().push_back(fn); }
+}  // namespace gcnb
+
+extern "C" int gcnb_set_watchdog_ms(int64_t ms) {
+  GCNB_REQUIRE(ms >= 0, "watchdog: negative limit");
+  for (auto fn : gcnb::watchdog_setters())
+    if (fn((unsigned long long)ms * 1000000ull) != 0) return gcnb::set_error(GCNB_ECUDA, "watchdog: symbol copy failed");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_version(void) { return 200; }  // 0.2.0
 
 extern "C" uint64_t gcnb_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 

@@ -21,15 +21,13 @@
 #include <cstdio>
 
 #include "common.cuh"
+#include "sync.cuh"
 
 namespace gcnb {
 
 namespace {
 
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
 // Canonical K-major, no-swizzle shared-memory matrix descriptor (sm_100):
 // start>>4 [0,14), LBO>>4 [16,30) (next 16-byte K chunk), SBO>>4 [32,46)
@@ -57,29 +55,6 @@ __device__ __forceinline__ void mma_commit(uint32_t mbar) {
                : "memory");
 }
 
-// Parity wait with a watchdog: a phase that never completes (a pipeline bug)
-// traps after ~4 s instead of hanging the device.
-__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
-  uint64_t t0 = 0;
-  for (;;) {
-    uint32_t done;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(mbar), "r"(parity)
-        : "memory");
-    if (done) return;
-    uint64_t now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    if (t0 == 0) {
-      t0 = now;
-    } else if (now - t0 > 4000000000ull) {
-      printf("gcnb: mbarrier wait timed out (block %d thread %d bar 0x%x parity %u)\n", blockIdx.x, threadIdx.x,
-             mbar, parity);
-      __trap();
-    }
-  }
-}
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -146,13 +121,7 @@ constexpr int DT_MAX_STAGES = 4;
 
 namespace {
 
-__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
-}
 
-__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
-}
 
 // D (tmem) (+)= A (tmem) · B (smem descriptor), kind::tf32
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
@@ -163,18 +132,7 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
 
-__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
-}
 
-// TMA: box at (x, y) of a 2-D tensor map into shared memory, completion counted on mbar
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t mbar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(mbar)
-      : "memory");
-}
 
 // X rows [m0, m0+N) (through the row list) into a K-major SWIZZLE_128B tile.
 __device__ __forceinline__ void load_x_rows(uint32_t stage, const float* __restrict__ X, int ldx,
@@ -532,6 +490,8 @@ EncodeTiledFn encode_tiled() {
   return fn;
 }
 
+}  // namespace
+
 // 2-D fp32 tensor map: dim0 = `cols` contiguous floats, dim1 = `n_rows` rows
 // `ld` floats apart; box {box0, box1}; out-of-range elements read as zero.
 bool tmap_2d(CUtensorMap* m, const float* base, int cols, int n_rows, int ld, int box0, int box1,
@@ -546,7 +506,6 @@ bool tmap_2d(CUtensorMap* m, const float* base, int cols, int n_rows, int ld, in
             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-}  // namespace
 
 int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
                     float* y, int ldy, int act, cudaStream_t st, const float* w_nk, int ld_wnk, const float* hmask,

@@ -36,7 +36,7 @@ def test_library_is_sm100a():
 
 def test_version_and_counter():
     lib = _lib.load()
-    assert lib.gcnb_version() == 100
+    assert lib.gcnb_version() == 200
     assert _lib.launch_count() >= 0
 
 
