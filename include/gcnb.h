@@ -98,6 +98,8 @@ int gcnb_spmm_f32(const int32_t* row_ptr, const int32_t* col, const float* val,
 int gcnb_window_csr(const int32_t* row_ptr, const int32_t* col, const float* val, int32_t n_rows,
                     int32_t n_own, int32_t bt, int32_t* nnear, void* entries, void* stream);
 int gcnb_aggwin_applies(int32_t d, int32_t bt, int32_t* out);
+/* measurement knob: which passes gcnb_aggwin_f32 runs (1 near, 2 far, 3 both = default) */
+int gcnb_set_aggwin_passes(int32_t mask);
 int gcnb_aggwin_f32(const int32_t* row_ptr, const int32_t* nnear, const void* entries, int32_t n_rows,
                     int32_t bt, const float* x, int32_t ldx, int32_t d, float* y, int32_t ldy, int32_t act,
                     void* stream);

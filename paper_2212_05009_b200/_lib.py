@@ -46,6 +46,7 @@ _SIGNATURES = {
     "gcnb_spmm_f32": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp]),
     "gcnb_window_csr": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
     "gcnb_aggwin_applies": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_int)]),
+    "gcnb_set_aggwin_passes": (_c_int, [_c_int]),
     "gcnb_aggwin_f32": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp]),
     "gcnb_pack_rows_f32": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _vp, _c_int, _vp, _vp, _vp]),
     "gcnb_wait_flags": (_c_int, [_vp, _vp, _c_int, _vp, _vp, _c_int, _vp]),

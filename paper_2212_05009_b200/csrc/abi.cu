@@ -49,7 +49,7 @@ int num_sms() {
 
 // Zero-initialised at module load on every device; a kernel that takes a
 // slot leaves it zero when it finishes (see k_agg).
-constexpr int SCHED_SLOTS = 1024;
+constexpr int SCHED_SLOTS = 4096;
 __device__ int g_sched[2 * SCHED_SLOTS];
 
 int* sched_counter(cudaStream_t st) {
@@ -71,10 +71,22 @@ int* sched_counter(cudaStream_t st) {
     }
     base[dev] = static_cast<int*>(p);
   }
+  // A launch captured into a CUDA graph gets a slot of its own (baked into that
+  // graph node, never shared): graphs captured on one stream and replayed
+  // concurrently on different streams then never race on a counter.  Eager
+  // launches share one slot per (device, stream): stream order serialises them.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) cudaGetLastError();
   auto key = std::make_pair(dev, st);
   auto it = slot_of.find(key);
   int slot;
-  if (it != slot_of.end()) {
+  if (cap == cudaStreamCaptureStatusActive) {
+    if (next_slot[dev] >= SCHED_SLOTS) {
+      set_error(GCNB_EINVAL, "more than %d captured or per-stream dynamically scheduled launches", SCHED_SLOTS);
+      return nullptr;
+    }
+    slot = next_slot[dev]++;
+  } else if (it != slot_of.end()) {
     slot = it->second;
   } else {
     if (next_slot[dev] >= SCHED_SLOTS) {

@@ -81,8 +81,15 @@ __device__ __forceinline__ float4 lds4_pred(uint32_t addr, bool pred) {
 
 __host__ __device__ constexpr int aw_ring_tiles(int bt) { return 2 * bt + 3; }
 
+constexpr int SE = 16;  // near entries staged per row group and pass
+
+// per-warp entry staging: 2 passes × GPW groups × (SE + 1) int2 (the +1 pad
+// spreads the groups' broadcast reads over different banks)
+__host__ __device__ constexpr int aw_stage_int2(int cs) { return (AW_WARPS - 1) * 2 * (32 / cs) * (SE + 1); }
+
 __host__ __device__ inline size_t aw_smem_bytes(int cs, int bt) {
-  return (size_t)aw_ring_tiles(bt) * AW_T * cs * 16 + (size_t)(aw_ring_tiles(bt) + AW_EMPTY) * 8 + 16;
+  return (size_t)aw_ring_tiles(bt) * AW_T * cs * 16 + (size_t)aw_stage_int2(cs) * 8 +
+         (size_t)(aw_ring_tiles(bt) + AW_EMPTY) * 8 + 16;
 }
 
 // First tile of range j: smallest tile whose first row starts at or after
@@ -103,15 +110,16 @@ __device__ __forceinline__ int range_bound(const int* __restrict__ rp, int n_row
 
 template <int CS>
 __global__ void __launch_bounds__(AW_THREADS, 1)
-    k_aggwin(const __grid_constant__ CUtensorMap xmap, const float4* __restrict__ X4, int ldx4, int c4,
-             const int* __restrict__ rp, const int* __restrict__ nnear, const int2* __restrict__ ent, int n_rows,
-             int n_ranges, int n_slices, int bt, float4* __restrict__ Y4, int ldy4, int act) {
+    k_aggwin(const __grid_constant__ CUtensorMap xmap, int c4, const int* __restrict__ rp,
+             const int* __restrict__ nnear, const int2* __restrict__ ent, int n_rows, int n_ranges, int n_slices,
+             int bt, float4* __restrict__ Y4, int ldy4) {
   constexpr int G = CS;          // lanes per row group (one float4 chunk each)
   constexpr int GPW = 32 / G;    // row groups per warp
   const int RT = aw_ring_tiles(bt);
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t ring = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)RT * AW_T * CS * 16);
+  int2* stage = reinterpret_cast<int2*>(smem + (size_t)RT * AW_T * CS * 16);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + aw_stage_int2(CS));
   const uint32_t full0 = smem_u32(bars);               // RT ring-slot barriers
   const uint32_t empty0 = smem_u32(bars + RT);          // AW_EMPTY tile-release barriers
   int* next = reinterpret_cast<int*>(bars + RT + AW_EMPTY);
@@ -159,23 +167,44 @@ __global__ void __launch_bounds__(AW_THREADS, 1)
     return;
   }
 
-  // consumers
+  // consumers (near pass): a group of G = CS lanes per row, GPW rows per
+  // warp.  A row's near entries are staged SE at a time in the warp's slice of
+  // shared memory (loaded one pass ahead into registers, then stored), and read
+  // back as broadcast LDS.64 — no shuffles, so no warp-convergence
+  // requirement inside the loops — then each lane reads its 16-byte chunk of
+  // the neighbour row from the ring (LDS.128).  No global data loads here:
+  // the far entries are the second pass (launch_agg_far).
   const int g = lane / G, gl = lane - g * G;
   const bool lane_on = g < GPW;
   const int q = c0 + gl;
   const bool q_on = lane_on && q < c4;
   const int row0 = ta * AW_T, row_end = tb * AW_T;
   const uint32_t ring_q = ring + (uint32_t)gl * 16;
+  int2* wst = stage + (size_t)warp * 2 * GPW * (SE + 1);
   int vhi = d_first - 1;  // highest data tile this warp has seen complete
-  for (;;) {
+  auto grab = [&]() {
     int b = 0;
     if (lane == 0) b = atomicAdd(next, GPW);
-    b = __shfl_sync(0xffffffffu, b, 0) + row0;
-    if (b >= row_end) break;
+    return __shfl_sync(0xffffffffu, b, 0) + row0;
+  };
+  auto extent = [&](int b, int& s, int& nn) {
+    const int r = b + g;
+    s = nn = 0;
+    if (lane_on && b < row_end && r < min(row_end, n_rows)) {
+      s = __ldg(rp + r);
+      nn = __ldg(nnear + r);
+    }
+  };
+  constexpr int JE = (SE + G - 1) / G;
+  int b = grab();
+  int s, nn;
+  extent(b, s, nn);
+  while (b < row_end) {
+    const int b_n = grab();  // the near pass is short: the next batch's extent is fetched now
+    int s_n, nn_n;
+    extent(b_n, s_n, nn_n);
     const int r = b + g;
     const bool r_in = lane_on && r < row_end;   // counts toward its tile's release
-    const bool r_real = r_in && r < n_rows;
-    // every data tile the batch's windows touch must have landed
     {
       const int t_lo = b / AW_T;
       const int t_hi = (min(b + GPW, row_end) - 1) / AW_T;
@@ -184,42 +213,50 @@ __global__ void __launch_bounds__(AW_THREADS, 1)
         mbar_wait(full0 + 8 * (d % RT), (uint32_t)((d - d_first) / RT) & 1u);
       vhi = max(vhi, dneed);
     }
-    int s = 0, nn = 0, nf = 0;
-    if (r_real) {
-      s = __ldg(rp + r);
-      nn = __ldg(nnear + r);
-      nf = __ldg(rp + r + 1) - s - nn;
-    }
     const int2* er = ent + s;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    // near entries: shared-memory ring
-    const int mn = __reduce_max_sync(0xffffffffu, nn);
-    for (int i = 0; i < mn; i += 4) {
-      int2 e[4];
+    const int maxnn = __reduce_max_sync(0xffffffffu, nn);
+    int2 e[JE];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) e[u] = (i + u < nn) ? ldg_int2(er + i + u) : make_int2(0, 0);
-      float4 x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = lds4_pred(ring_q + (uint32_t)e[u].x * (CS * 16), q_on && i + u < nn);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc = fma4(__int_as_float(e[u].y), x[u], acc);
+    for (int j = 0; j < JE; ++j) {
+      const int k = j * G + gl;
+      e[j] = (k < SE && k < nn) ? ldg_int2(er + k) : make_int2(0, 0);
     }
-    // far entries: global gathers, 8 in flight per lane
-    const int mf = __reduce_max_sync(0xffffffffu, nf);
-    const int2* ef = er + nn;
-    for (int i = 0; i < mf; i += 8) {
-      int2 e[8];
+    for (int base = 0; base < maxnn; base += SE) {
+      int2* buf = wst + ((base / SE) & 1) * GPW * (SE + 1) + g * (SE + 1);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) e[u] = (i + u < nf) ? ldg_int2(ef + i + u) : make_int2(0, 0);
-      float4 x[8];
+      for (int j = 0; j < JE; ++j) {
+        const int k = j * G + gl;
+        if (lane_on && k < SE) buf[k] = e[j];
+      }
+      if (base + SE < maxnn) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = ldg4_pred(X4 + (size_t)e[u].x * ldx4 + q, q_on && i + u < nf);
+        for (int j = 0; j < JE; ++j) {
+          const int k = base + SE + j * G + gl;
+          e[j] = (j * G + gl < SE && k < nn) ? ldg_int2(er + k) : make_int2(0, 0);
+        }
+      }
+      __syncwarp();
+      const int cnt = min(SE, maxnn - base);
+      for (int kk = 0; kk < cnt; kk += 4) {
+        int2 t[4];
+        float4 x[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc = fma4(__int_as_float(e[u].y), x[u], acc);
+        for (int u = 0; u < 4; ++u) t[u] = (kk + u < SE) ? buf[kk + u] : make_int2(0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          x[u] = lds4_pred(ring_q + (uint32_t)t[u].x * (CS * 16), q_on && base + kk + u < nn);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc = fma4(__int_as_float(t[u].y), x[u], acc);
+      }
+      __syncwarp();
     }
-    if (r_real && q_on) Y4[(size_t)r * ldy4 + q] = act >= 0 ? act_fwd4(acc, act) : acc;
-    // release the row (its ring reads are done: the FMAs consumed them)
+    // release the row's ring data, store the near partial sum (the far pass adds the rest)
     if (r_in && gl == 0) mbar_arrive(empty0 + 8 * (((r / AW_T) - ta) % AW_EMPTY));
+    if (r_in && r < n_rows && q_on) Y4[(size_t)r * ldy4 + q] = acc;
+    b = b_n;
+    s = s_n;
+    nn = nn_n;
   }
 }
 
@@ -261,6 +298,10 @@ __global__ void k_wincsr(const int* __restrict__ rp, const int* __restrict__ col
 }
 
 }  // namespace
+
+// Passes gcnb_aggwin_f32 runs (bit 0 near, bit 1 far): a measurement knob
+// (gcnb_set_aggwin_passes), 3 = both = the aggregation.
+int g_aggwin_passes = 3;
 
 // Chunk count per slice for a row of c4 float4 chunks.
 static int aggwin_cs(int c4) { return (c4 % 5 == 0 && c4 % 4 != 0) ? 5 : 4; }
@@ -312,9 +353,17 @@ extern "C" int gcnb_aggwin_f32(const int32_t* row_ptr, const int32_t* nnear, con
   cudaStream_t st = (cudaStream_t)stream;
   auto fn = cs == 5 ? k_aggwin<5> : k_aggwin<4>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fn<<<n_ranges * n_slices, AW_THREADS, smem, st>>>(map, reinterpret_cast<const float4*>(x), ldx / 4, c4, row_ptr,
-                                                    nnear, static_cast<const int2*>(entries), n_rows, n_ranges,
-                                                    n_slices, bt, reinterpret_cast<float4*>(y), ldy / 4, act);
-  GCNB_AFTER_LAUNCH("aggregation (windowed)");
+  if (!(g_aggwin_passes & 1)) return (g_aggwin_passes & 2) ? launch_agg_far(row_ptr, nnear, entries, n_rows, x, ldx, d, y, ldy, act, st) : GCNB_OK;
+  fn<<<n_ranges * n_slices, AW_THREADS, smem, st>>>(map, c4, row_ptr, nnear, static_cast<const int2*>(entries),
+                                                    n_rows, n_ranges, n_slices, bt, reinterpret_cast<float4*>(y),
+                                                    ldy / 4);
+  GCNB_AFTER_LAUNCH("aggregation (windowed, near pass)");
+  if (!(g_aggwin_passes & 2)) return GCNB_OK;
+  return launch_agg_far(row_ptr, nnear, entries, n_rows, x, ldx, d, y, ldy, act, st);
+}
+
+extern "C" int gcnb_set_aggwin_passes(int32_t mask) {
+  GCNB_REQUIRE(mask >= 0 && mask <= 3, "aggwin passes: mask in [0, 3]");
+  gcnb::g_aggwin_passes = mask;
   return GCNB_OK;
 }

@@ -27,6 +27,10 @@ int num_sms();
 // concurrently on different streams never share a counter.
 int* sched_counter(cudaStream_t st);
 
+// rowops.cu: far pass of the windowed aggregation (aggwin.cu) — k_agg over the
+// far int2 entries of each row, added to the near partial sums in y, then act.
+int launch_agg_far(const int32_t* row_ptr, const int32_t* nnear, const void* entries, int32_t n_rows, const float* x,
+                   int32_t ldx, int32_t d, float* y, int32_t ldy, int32_t act, cudaStream_t st);
 // dense.cu: register-blocked SIMT transform for the wide dense layers
 bool dense_blocked_applies(int d_in, int d_out);
 int launch_dense_blocked(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,

@@ -53,24 +53,22 @@ __device__ __forceinline__ void row_extent(const int* __restrict__ rp, int row, 
 // the current chunk's gathers are issued, so the index stream and the
 // feature-row gathers overlap instead of forming two dependent round trips
 // per chunk.
-template <int LPR, int VPL>
+template <bool ENT>
+__device__ __forceinline__ void load_nz(const int* __restrict__ col, const float* __restrict__ val, int e, int& c,
+                                        float& v);
+
+template <int LPR, int VPL, bool ENT = false>
 __device__ __forceinline__ void aggregate_span(const int* __restrict__ col, const float* __restrict__ val, int s,
                                                int len, const float4* __restrict__ X4, int ldx4, int c4, int gl,
                                                float4 (&acc)[VPL]) {
   const int maxlen = __reduce_max_sync(0xffffffffu, len);
   int cj = 0;
   float vj = 0.0f;
-  if (gl < len) {
-    cj = __ldg(col + s + gl);
-    vj = __ldg(val + s + gl);
-  }
+  if (gl < len) load_nz<ENT>(col, val, s + gl, cj, vj);
   for (int base = 0; base < maxlen; base += LPR) {
     int cn = 0;
     float vn = 0.0f;
-    if (base + LPR + gl < len) {
-      cn = __ldg(col + s + base + LPR + gl);
-      vn = __ldg(val + s + base + LPR + gl);
-    }
+    if (base + LPR + gl < len) load_nz<ENT>(col, val, s + base + LPR + gl, cn, vn);
     const int cnt = min(LPR, maxlen - base);
     // Issue U independent row gathers into distinct registers before any is
     // consumed: a load→fma→load chain would keep only one gather in flight
@@ -130,7 +128,22 @@ __device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src
         : "memory");
 }
 
-template <int LPR, int VPL, int U, bool CA = false>
+// (column, value) of nonzero e: separate CSR arrays, or (ENT) the int2
+// {column, value bits} entries of the windowed layout (aggwin.cu).
+template <bool ENT>
+__device__ __forceinline__ void load_nz(const int* __restrict__ col, const float* __restrict__ val, int e, int& c,
+                                        float& v) {
+  if constexpr (ENT) {
+    const int2 t = __ldg(reinterpret_cast<const int2*>(col) + e);
+    c = t.x;
+    v = __int_as_float(t.y);
+  } else {
+    c = __ldg(col + e);
+    v = __ldg(val + e);
+  }
+}
+
+template <int LPR, int VPL, int U, bool CA = false, bool ENT = false>
 __device__ __forceinline__ void aggregate_span_cp(const int* __restrict__ col, const float* __restrict__ val, int s,
                                                   int len, const float4* __restrict__ X4, int ldx4, int c4, int gl,
                                                   float4 (&acc)[VPL], float4* __restrict__ stage) {
@@ -138,17 +151,11 @@ __device__ __forceinline__ void aggregate_span_cp(const int* __restrict__ col, c
   const int maxlen = __reduce_max_sync(0xffffffffu, len);
   int cj = 0;
   float vj = 0.0f;
-  if (gl < len) {
-    cj = __ldg(col + s + gl);
-    vj = __ldg(val + s + gl);
-  }
+  if (gl < len) load_nz<ENT>(col, val, s + gl, cj, vj);
   for (int base = 0; base < maxlen; base += LPR) {
     int cn = 0;
     float vn = 0.0f;
-    if (base + LPR + gl < len) {
-      cn = __ldg(col + s + base + LPR + gl);
-      vn = __ldg(val + s + base + LPR + gl);
-    }
+    if (base + LPR + gl < len) load_nz<ENT>(col, val, s + base + LPR + gl, cn, vn);
     const int cnt = min(LPR, maxlen - base);
     for (int t0 = 0; t0 < cnt; t0 += U) {
       float vv[U];
@@ -213,12 +220,15 @@ __host__ __device__ constexpr int agg_batch(int lpr, int vpl) {
 // on the stream.
 constexpr int AGG_ROWS_PER_GRAB = 4;
 
-template <int LPR, int VPL>
+// FAR: the second pass of the windowed aggregation (aggwin.cu): only the far
+// entries [rp[r] + nnear[r], rp[r+1]) of the int2 entry array (`col`), added to
+// the near partial sum already in Y (order: near entries, then far entries).
+template <int LPR, int VPL, bool FAR = false>
 __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const int* __restrict__ col,
                                             const float* __restrict__ val, const int* __restrict__ rows,
                                             int n_rows, const float4* __restrict__ X4, int ldx4, int c4,
                                             float4* __restrict__ Y4, int ldy4, int act, int* __restrict__ sched,
-                                            int regs) {
+                                            int regs, const int* __restrict__ nnear) {
   constexpr int GPW = 32 / LPR;
   constexpr int CH = AGG_ROWS_PER_GRAB > GPW ? AGG_ROWS_PER_GRAB / GPW : 1;  // row groups per grab
   constexpr int RPG = GPW * CH;                                                // rows per grab
@@ -238,10 +248,18 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
     const int i = b + c * GPW + gw;
     return (b < n_rows && i < n_rows) ? (rows ? __ldg(rows + i) : i) : -1;
   };
+  auto extent = [&](int row, int& s, int& len) {
+    row_extent(rp, row, s, len);
+    if (FAR && row >= 0) {
+      const int nn = __ldg(nnear + row);
+      s += nn;
+      len -= nn;
+    }
+  };
   int base = grab(), c = 0;
   int row = row_of(base, 0);
   int s, len;
-  row_extent(rp, row, s, len);
+  extent(row, s, len);
   while (base < n_rows) {
     // next row group (grabbing the next chunk one row early), its extent
     // prefetched while this row is aggregated
@@ -252,13 +270,16 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
     }
     const int row_n = row_of(base_n, c_n);
     int s_n, len_n;
-    row_extent(rp, row_n, s_n, len_n);
+    extent(row_n, s_n, len_n);
     float4 acc[VPL];
 #pragma unroll
-    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (regs == 1) aggregate_span<LPR, VPL>(col, val, s, len, X4, ldx4, c4, gl, acc);
-    else if (regs == 2) aggregate_span_cp<LPR, VPL, U, true>(col, val, s, len, X4, ldx4, c4, gl, acc, stage);
-    else aggregate_span_cp<LPR, VPL, U>(col, val, s, len, X4, ldx4, c4, gl, acc, stage);
+    for (int q = 0; q < VPL; ++q) {
+      acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (FAR && row >= 0 && gl + q * LPR < c4) acc[q] = Y4[(size_t)row * ldy4 + gl + q * LPR];
+    }
+    if (regs == 1) aggregate_span<LPR, VPL, FAR>(col, val, s, len, X4, ldx4, c4, gl, acc);
+    else if (regs == 2) aggregate_span_cp<LPR, VPL, U, true, FAR>(col, val, s, len, X4, ldx4, c4, gl, acc, stage);
+    else aggregate_span_cp<LPR, VPL, U, false, FAR>(col, val, s, len, X4, ldx4, c4, gl, acc, stage);
     if (row >= 0) {
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
@@ -660,7 +681,7 @@ int tile_rows(int d_out, int lpr, int* rpt_out) {
 #define GCNB_LPR_CASES(M) M(2, 1) M(4, 1) M(8, 1) M(16, 1) M(32, 1) M(32, 2)
 
 using AggFn = void (*)(const int*, const int*, const float*, const int*, int, const float4*, int, int, float4*, int,
-                       int, int*, int);
+                       int, int*, int, const int*);
 // Shape of the aggregation-only kernel over all own rows: two float4 chunks per
 // lane from 9 chunks up, so 2-4 rows share a warp (rows of similar length side by
 // side after the degree-sorted layout windows): measured on the products shape,
@@ -675,8 +696,8 @@ AggShape agg_shape_spmm(int d) {
 }
 
 #define GCNB_AGG_EXTRA_CASES(M) M(4, 3) M(8, 2) M(8, 4) M(16, 2)
-AggFn pick_agg(AggShape s) {
-#define M(L, V) if (s.lpr == L && s.vpl == V) return k_agg<L, V>;
+AggFn pick_agg(AggShape s, bool far = false) {
+#define M(L, V) if (s.lpr == L && s.vpl == V) return far ? k_agg<L, V, true> : k_agg<L, V, false>;
   GCNB_LPR_CASES(M)
   GCNB_AGG_EXTRA_CASES(M)
 #undef M
@@ -778,12 +799,12 @@ int check_csr_args(const int32_t* row_ptr, const int32_t* col, const float* val,
 
 int launch_agg(const int32_t* row_ptr, const int32_t* col, const float* val, const int32_t* rows, int32_t n_rows,
                const float* x, int32_t ldx, int32_t d, float* y, int32_t ldy, int32_t act, cudaStream_t st,
-               const char* what) {
+               const char* what, const int32_t* nnear = nullptr) {
   // row lists (interior / boundary rows of an overlapped exchange) keep one row
   // group per 16-32 lanes: pairing rows of a list measured slower at 2-4 GPUs
   AggShape s = rows ? agg_shape(d) : agg_shape_spmm(d);
   if (g_agg_lpr > 0 && g_agg_lpr * g_agg_vpl * 4 >= round4(d)) s = {g_agg_lpr, g_agg_vpl};
-  AggFn fn = pick_agg(s);
+  AggFn fn = pick_agg(s, nnear != nullptr);
   GCNB_REQUIRE(fn != nullptr, "%s: no aggregation kernel for lpr=%d vpl=%d", what, s.lpr, s.vpl);
   const size_t smem = (size_t)WARPS * agg_batch(s.lpr, s.vpl) * s.vpl * 32 * sizeof(float4);
   const int rows_per_block = NT / s.lpr;
@@ -799,7 +820,7 @@ int launch_agg(const int32_t* row_ptr, const int32_t* col, const float* val, con
   int* sched = sched_counter(st);
   GCNB_REQUIRE(sched != nullptr, "%s: no work-counter slot for this stream", what);
   fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, reinterpret_cast<const float4*>(x), ldx / 4,
-                             round4(d) / 4, reinterpret_cast<float4*>(y), ldy / 4, act, sched, g_agg_regs);
+                             round4(d) / 4, reinterpret_cast<float4*>(y), ldy / 4, act, sched, g_agg_regs, nnear);
   GCNB_AFTER_LAUNCH(what);
   return GCNB_OK;
 }
@@ -822,6 +843,13 @@ int launch_fwd_gemm(bool agg, const int32_t* row_ptr, const int32_t* col, const 
 }
 
 }  // namespace
+
+int launch_agg_far(const int32_t* row_ptr, const int32_t* nnear, const void* entries, int32_t n_rows, const float* x,
+                   int32_t ldx, int32_t d, float* y, int32_t ldy, int32_t act, cudaStream_t st) {
+  return launch_agg(row_ptr, static_cast<const int32_t*>(entries), nullptr, nullptr, n_rows, x, ldx, d, y, ldy, act,
+                    st, "aggregation (windowed, far pass)", nnear);
+}
+
 }  // namespace gcnb
 
 using namespace gcnb;

@@ -397,7 +397,7 @@ class DistributedTrainer:
 # bench entry (launched by torchrun, one process per GPU)
 
 
-def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summary, cpu_epoch_timer, METRIC, UNIT):
+def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summary, _unused, METRIC, UNIT):
     import torch
     import torch.distributed as dist
 
@@ -600,7 +600,8 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
         "gpu_launches": int(launches * args.steps),
         "roofline": {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                     "algo_bytes_per_launch": kbytes, "ms_per_launch": round(kms, 5)},
+                     "bytes_per_launch": kbytes, "bytes_kind": "compulsory", "ms_per_launch": round(kms, 5),
+                     "gather_gbs": table.get(kname, {}).get("gather_gbs")},
         "kernels": table,
         "halo_bytes_per_epoch": int(halo[0].item()), "reference_words_per_epoch": int(halo[1].item()),
         "exposed_comm_pct": round(100.0 * max(0.0, ms - msc) / ms, 2), "compute_only_ms": round(msc, 4),

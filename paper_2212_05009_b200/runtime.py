@@ -23,6 +23,7 @@ no layer < k reads W^k.
 
 from __future__ import annotations
 
+import os
 import queue
 import threading
 from dataclasses import dataclass
@@ -168,6 +169,17 @@ def allreduce_sum(contributions) -> np.ndarray:
 # per-rank device state
 
 
+# Windowed aggregation (csrc/aggwin.cu): half-width of the shared-memory row
+# window in 128-row tiles, minimum row-block size, and the switch.  Off by
+# default: on the products shape it measured slower than the row-gather kernel
+# (6.6 vs 3.45 ms for d=100 — 61 % of the nonzeros fall in the
+# window, the shared-memory pass is wavefront-bound at ~1.8x its ideal and the
+# far pass alone costs half of the row-gather kernel); GCNB_AGGWIN=1 enables it.
+WINDOW_TILES = 8
+WINDOW_MIN_ROWS = 1 << 15
+WINDOW_ON = os.environ.get("GCNB_AGGWIN", "0") == "1"
+
+
 class _DeviceOp:
     """Device copy of one OpLayout."""
 
@@ -180,9 +192,49 @@ class _DeviceOp:
         lens = np.diff(lay.row_ptr)
         self._nnz = {"all": int(lay.row_ptr[-1]), "interior": int(lens[lay.interior].sum()),
                      "boundary": int(lens[lay.boundary].sum())}
+        self.dev = dev
+        self.win = None  # (nnear, entries) of the windowed aggregation
+        if WINDOW_ON and lay.n_own >= WINDOW_MIN_ROWS:
+            with torch.cuda.device(dev):
+                self.window()  # built here, never inside a graph capture
+
+    def window(self):
+        """Near-first int2 entries for gcnb_aggwin_f32 (gcnb_window_csr; built once,
+        on the device, from the uploaded CSR)."""
+        if self.win is None:
+            n = self.lay.n_own
+            nnear = torch.zeros(max(n, 1), dtype=torch.int32, device=self.dev)
+            ent = torch.zeros((max(self.csr.nnz, 1), 2), dtype=torch.int32, device=self.dev)
+            _lib.call("gcnb_window_csr", self.csr.row_ptr.data_ptr(), self.csr.col.data_ptr(),
+                      self.csr.val.data_ptr(), n, n, WINDOW_TILES, nnear.data_ptr(), ent.data_ptr(),
+                      torch.cuda.current_stream(self.dev).cuda_stream)
+            self.win = (nnear, ent)
+        return self.win
+
+    def use_window(self, rows: str, width: int) -> bool:
+        """The windowed (shared-memory) aggregation runs for whole row blocks of
+        at least WINDOW_MIN_ROWS rows and widths it supports."""
+        return (WINDOW_ON and rows == "all" and self.lay.n_own >= WINDOW_MIN_ROWS
+                and _lib.aggwin_applies(width, WINDOW_TILES))
+
+    def aggregate_all(self, x, width: int, y, act: int, stream) -> None:
+        """y[r] = act(Σ_j A[r,j]·x[j]) for all own rows, windowed kernel."""
+        nnear, ent = self.window()
+        _lib.call("gcnb_aggwin_f32", self.csr.row_ptr.data_ptr(), nnear.data_ptr(), ent.data_ptr(),
+                  self.lay.n_own, WINDOW_TILES, x.data_ptr(), x.shape[1], width, y.data_ptr(), y.shape[1], act,
+                  stream)
 
     def nnz_of(self, rows: str) -> int:
         return self._nnz[rows]
+
+    def compulsory(self, rows: str, d_in: int, d_out: int) -> int:
+        """Compulsory HBM bytes of an aggregation over the row set: row_ptr,
+        (col, val) once, every operand row once (all n_cols = own + halo for
+        `all`; a row list's nnz share of them otherwise), one output row per row."""
+        n_sel = {"all": self.lay.n_own, "interior": len(self.lay.interior), "boundary": len(self.lay.boundary)}[rows]
+        nnz = self._nnz[rows]
+        n_x = self.lay.n_cols if rows == "all" else (self.lay.n_cols * nnz) // max(self._nnz["all"], 1)
+        return 4 * (n_sel + 1) + 8 * nnz + 4 * d_in * n_x + 4 * d_out * n_sel
 
 
 class _WeightList(list):
@@ -437,10 +489,13 @@ class ProcState:
             # fwd_finish(k) transforms all own rows at once (contiguous: TMA).
             ws = self.fwd_ws[k]
             with span(f"fwd{k}", 4 * (n_sel + 1) + 8 * nnz + 4 * width * nnz + 4 * width * n_sel, 2 * nnz * width,
-                      self.stream()):
-                _lib.call("gcnb_fwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
-                          op.csr.val.data_ptr(), sel, n_sel, x.data_ptr(), x.shape[1], width, 0, width,
-                          ws.data_ptr(), ws.shape[1], _lib.ACT["identity"], self.stream())
+                      self.stream(), op.compulsory(rows, width, width)):
+                if op.use_window(rows, width):
+                    op.aggregate_all(x, width, ws, _lib.ACT["identity"], self.stream())
+                else:
+                    _lib.call("gcnb_fwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
+                              op.csr.val.data_ptr(), sel, n_sel, x.data_ptr(), x.shape[1], width, 0, width,
+                              ws.data_ptr(), ws.shape[1], _lib.ACT["identity"], self.stream())
             if rows == "all":
                 self.fwd_finish(k)
             return
@@ -449,7 +504,11 @@ class ProcState:
         if fused:
             algo += 4 * width * d_out
             flops += 2 * n_sel * width * d_out
-        with span(f"fwd{k}", algo, flops, self.stream()):
+        with span(f"fwd{k}", algo, flops, self.stream(),
+                  op.compulsory(rows, width, d_out) + (4 * width * d_out if fused else 0)):
+            if not fused and op.use_window(rows, width):
+                op.aggregate_all(x, width, h, self.act, self.stream())
+                return
             _lib.call("gcnb_fwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
                       op.csr.val.data_ptr(), sel, n_sel, x.data_ptr(), x.shape[1], width, w, d_out, h.data_ptr(),
                       h.shape[1], self.act, self.stream())
@@ -523,10 +582,13 @@ class ProcState:
             op_nnz = op.nnz_of(rows)
             ws = self.bwd_ws[k]
             with span(f"bwd{k}", 4 * (n_sel + 1) + 8 * op_nnz + 4 * self.dims[k] * (op_nnz + n_sel), 2 * op_nnz *
-                      self.dims[k], self.stream()):
-                _lib.call("gcnb_spmm_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(), op.csr.val.data_ptr(),
-                          sel, n_sel, g.data_ptr(), g.shape[1], self.dims[k], ws.data_ptr(), ws.shape[1],
-                          self.stream())
+                      self.dims[k], self.stream(), op.compulsory(rows, self.dims[k], self.dims[k])):
+                if op.use_window(rows, self.dims[k]):
+                    op.aggregate_all(g, self.dims[k], ws, -1, self.stream())
+                else:
+                    _lib.call("gcnb_spmm_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
+                              op.csr.val.data_ptr(), sel, n_sel, g.data_ptr(), g.shape[1], self.dims[k],
+                              ws.data_ptr(), ws.shape[1], self.stream())
             return self.bwd_finish(k) if rows == "all" else 0
         hp = self.hbuf[k - 1]
         gp = self.gext[k - 1] if k > 1 else None
@@ -538,7 +600,10 @@ class ProcState:
         if gp is not None:
             algo += 4 * dp * n_sel + 4 * dp * dk
             flops += 2 * n_sel * dp * dk
-        with span(f"bwd{k}", algo, flops, self.stream()):
+        comp = op.compulsory(rows, dk, 0) + 4 * dp * n_sel + 4 * dp * dk * used
+        if gp is not None:
+            comp += 4 * dp * n_sel + 4 * dp * dk
+        with span(f"bwd{k}", algo, flops, self.stream(), comp):
             _lib.call("gcnb_bwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
                       op.csr.val.data_ptr(), sel, n_sel, g.data_ptr(), g.shape[1], dk, hp.data_ptr(), hp.shape[1],
                       dp, self.w[k].data_ptr(), 0 if gp is None else gp.data_ptr(),

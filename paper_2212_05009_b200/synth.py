@@ -27,19 +27,32 @@ is deterministic in `seed` and documented in BASELINE.md §4 / DESIGN.md §6.
 
 from __future__ import annotations
 
+from typing import NamedTuple
+
 import numpy as np
 
-from .sparse import CsrMatrix
+# Pure numpy on purpose: bench.py's reference arm loads this file standalone
+# (no package import, no native library), so both arms time the same graph.
 
 
-def _csr_from_pairs(n: int, rows: np.ndarray, cols: np.ndarray) -> CsrMatrix:
+class RawPattern(NamedTuple):
+    """Unit-valued CSR pattern (wrap with sparse.CsrMatrix for the product path)."""
+
+    n_rows: int
+    n_cols: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+
+
+def _csr_from_pairs(n: int, rows: np.ndarray, cols: np.ndarray) -> RawPattern:
     """Distinct (row, col) pairs → unit-valued CSR (one int64 key sort)."""
     keys = np.asarray(rows, dtype=np.int64) * n + np.asarray(cols, dtype=np.int64)
     keys.sort()
     rows = keys // n
     rp = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
-    return CsrMatrix(n, n, rp, keys - rows * n, np.ones(len(keys)))
+    return RawPattern(n, n, rp, keys - rows * n, np.ones(len(keys)))
 
 
 def _uniq(x: np.ndarray) -> np.ndarray:
@@ -61,7 +74,7 @@ def _exact_count(keys: np.ndarray, m: int, rng) -> np.ndarray:
     return np.sort(keys[rng.choice(len(keys), size=m, replace=False)])
 
 
-def config1(seed: int = 0, n: int = 10_000, density: float = 0.001) -> CsrMatrix:
+def config1(seed: int = 0, n: int = 10_000, density: float = 0.001) -> RawPattern:
     rng = np.random.default_rng([seed, 0xD1])
     rows, cols = [], []
     chunk = 1000
@@ -78,7 +91,7 @@ def config1(seed: int = 0, n: int = 10_000, density: float = 0.001) -> CsrMatrix
 
 
 def amazon0601(seed: int = 0, n: int = 403_394, m: int = 3_387_388, mean_offset: float = 50.0,
-               shortcut: float = 0.02) -> CsrMatrix:
+               shortcut: float = 0.02) -> RawPattern:
     rng = np.random.default_rng([seed, 0xA0601])
     deg = rng.poisson(1.03 * m / n, n)
     src = np.repeat(np.arange(n, dtype=np.int64), deg)
@@ -91,7 +104,7 @@ def amazon0601(seed: int = 0, n: int = 403_394, m: int = 3_387_388, mean_offset:
     return _csr_from_pairs(n, perm[keys // n], perm[keys % n])
 
 
-def roadnet(seed: int = 0, side: int = 1404, kept_edges: int = 2_766_607) -> CsrMatrix:
+def roadnet(seed: int = 0, side: int = 1404, kept_edges: int = 2_766_607) -> RawPattern:
     rng = np.random.default_rng([seed, 0x20AD])
     n = side * side
     v = np.arange(n, dtype=np.int64).reshape(side, side)
@@ -106,7 +119,10 @@ def roadnet(seed: int = 0, side: int = 1404, kept_edges: int = 2_766_607) -> Csr
 
 def _searchsorted(cum: np.ndarray, x: np.ndarray) -> np.ndarray:
     """np.searchsorted(cum, x) (side='left'), threaded in csrc_host/csr.cpp when
-    the host library is built (identical results)."""
+    the host library is built (identical results).  Loaded standalone (the
+    reference arm), the relative import fails and numpy does it."""
+    if __package__ is None or not __package__:
+        return np.searchsorted(cum, x)
     try:
         from . import hp
 
@@ -122,7 +138,7 @@ def _searchsorted(cum: np.ndarray, x: np.ndarray) -> np.ndarray:
 
 
 def products(seed: int = 0, n: int = 2_449_029, pairs: int = 61_859_140, blocks: int = 2048,
-             intra: float = 0.8, sigma: float = 1.0, block_offset: float = 16.0) -> CsrMatrix:
+             intra: float = 0.8, sigma: float = 1.0, block_offset: float = 16.0) -> RawPattern:
     rng = np.random.default_rng([seed, 0x9200])
     block = np.sort(rng.integers(0, blocks, n))          # contiguous blocks before relabelling
     bounds = np.searchsorted(block, np.arange(blocks + 1))

@@ -68,6 +68,12 @@ for d in dims:
     same = bool(torch.equal(y1, y1b))
     t0 = timed(f0)
     t1 = timed(f1)
+    passes = []
+    for mask in (1, 2):
+        _lib.call("gcnb_set_aggwin_passes", mask)
+        passes.append(timed(f1)[0])
+    _lib.call("gcnb_set_aggwin_passes", 3)
+    print(f"d={d}: near pass {passes[0]:.3f} ms, far pass {passes[1]:.3f} ms", flush=True)
     comp = 4 * (n + 1) + 8 * nnz + 4 * d * 2 * n
     print(f"d={d}: spmm {t0[0]:.3f} ms (med {t0[1]:.3f}) | aggwin {t1[0]:.3f} ms (med {t1[1]:.3f}) "
           f"speed-up {t0[0] / t1[0]:.2f}x | max err/max {err:.2e} rerun-identical {same} | "
