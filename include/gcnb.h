@@ -234,6 +234,17 @@ int gcnb_loss_grad_f32(const float* h, int32_t ldh, int32_t n_rows, int32_t d,
                        const int32_t* label, double inv_n_labeled,
                        float* g, int32_t ldg, int32_t act,
                        double* scratch, double* loss_sum, void* stream);
+/* gcnb_loss_grad_f32 with the backward halo pack of the last layer fused into
+ * its epilogue (north_star subsystem 2; runtime.py:336-341 + SimNetwork.send):
+ * every G row is also stored into the receivers' halo slots the plan assigns
+ * to it — map[map_ptr[r] .. map_ptr[r+1]) = {segment s, position}, segment s
+ * = receiver halo block dst[s] (row stride ldd floats) — and once all blocks'
+ * stores are visible the last block increments flags[s] (system-scope
+ * release), exactly as gcnb_pack_rows_f32 would after a separate launch. */
+int gcnb_loss_grad_pack_f32(const float* h, int32_t ldh, int32_t n_rows, int32_t d, const int32_t* label,
+                            double inv_n_labeled, float* g, int32_t ldg, int32_t act, double* scratch,
+                            double* loss_sum, const int32_t* map_ptr, const int32_t* map, float* const* dst,
+                            uint64_t* const* flags, int32_t n_seg, int32_t ldd, int32_t* counter, void* stream);
 
 /* allreduce_sum (runtime.py:147-157): out = bufs[0] + bufs[1] + ... in
  * ascending rank order (bit-identical on every rank).  bufs is a host array of
@@ -266,6 +277,32 @@ int gcnb_sgd_f32(float* w, const float* dw, int64_t n, float lr, void* stream);
  * for j < d, 0 for d <= j < ld_dst (host-prepared inputs uploaded as fp64). */
 int gcnb_cast_pad_f64_f32(const double* src, int32_t ld_src, int64_t n_rows,
                           int32_t d, float* dst, int32_t ld_dst, void* stream);
+
+/* ---- setup: device communication plan + rank layout ------
+ * gcnb_plan_build = comm.build_comm_plan (comm.py:59-93) for all ranks at once:
+ * CSR rp/ci (int64, n rows, square), owner (int32 n), p ranks.  Out: *keys_out
+ * = library-allocated sorted distinct keys (consumer << 56 | sender << 49 |
+ * column), so block (c, s) = pair_bounds[c*p+s] .. pair_bounds[c*p+s+1] is
+ * send[s][c] in ascending column order (and consumer c's blocks, in sender
+ * order, are its halo in the reference's positional order); rows_sorted =
+ * every rank's rows ascending, rank r's at rank_ptr[r] .. rank_ptr[r+1];
+ * localpos[v] = v's position among its owner's rows.  Free keys with
+ * gcnb_plan_free.  Synchronises `stream` (setup-time only).
+ * gcnb_layout_fill = one rank's block of scatter (runtime.py:203-275): the
+ * extended CSR over [own rows | halo] for own rows in `layout_rows` order
+ * (halo = keys[halo_k0 .. halo_k0+n_halo)), fp64 values, each row sorted by
+ * extended column when sort_rows and n_halo > 0; has_halo_out[i] = row i has a
+ * halo column (boundary row).  ext_col_out / val_out hold Σ row lengths. */
+int gcnb_plan_build(const int64_t* rp, const int64_t* ci, int64_t n, const int32_t* owner, int32_t p,
+                    uint64_t** keys_out, int64_t* n_keys_out, int64_t* pair_bounds, int32_t* rows_sorted,
+                    int32_t* rank_ptr, int32_t* localpos, void* stream);
+int gcnb_plan_free(void* keys);
+int gcnb_layout_fill(const int64_t* rp, const int64_t* ci, const double* val, int64_t n, const int32_t* layout_rows,
+                     int32_t n_own, const uint64_t* keys, int64_t halo_k0, int64_t n_halo, int32_t sort_rows,
+                     int64_t* row_ptr_out, int32_t* ext_col_out, double* val_out, int32_t* has_halo_out,
+                     int32_t* colmap_scratch, void* stream);
+/* synchronous device -> host copy (library-allocated buffers) */
+int gcnb_copy_d2h(void* dst_host, const void* src_dev, size_t bytes);
 
 #ifdef __cplusplus
 }

@@ -72,6 +72,9 @@ _SIGNATURES = {
     "gcnb_loss_scratch_doubles": (_c_int, []),
     "gcnb_loss_grad_f32": (
         _c_int, [_vp, _c_int, _c_int, _c_int, _vp, _f64, _vp, _c_int, _c_int, _vp, _vp, _vp]),
+    "gcnb_loss_grad_pack_f32": (
+        _c_int, [_vp, _c_int, _c_int, _c_int, _vp, _f64, _vp, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _c_int,
+                 _c_int, _vp, _vp]),
     "gcnb_sum_buffers_f32": (_c_int, [_vp, _c_int, _c_i64, _vp, _vp]),
     "gcnb_sum_buffers_f64": (_c_int, [_vp, _c_int, _c_i64, _vp, _vp]),
     "gcnb_sgd_f32": (_c_int, [_vp, _vp, _c_i64, _f32, _vp]),
@@ -79,6 +82,12 @@ _SIGNATURES = {
     "gcnb_sum_slots_f32": (_c_int, [_vp, _c_int, _c_i64, _c_i64, _vp, _vp, _vp]),
     "gcnb_signal_peers": (_c_int, [_vp, _c_int, _vp]),
     "gcnb_cast_pad_f64_f32": (_c_int, [_vp, _c_int, _c_i64, _c_int, _vp, _c_int, _vp]),
+    "gcnb_plan_build": (_c_int, [_vp, _vp, _c_i64, _vp, _c_int, ctypes.POINTER(_vp), ctypes.POINTER(_c_i64), _vp, _vp,
+                                 _vp, _vp, _vp]),
+    "gcnb_plan_free": (_c_int, [_vp]),
+    "gcnb_layout_fill": (_c_int, [_vp, _vp, _vp, _c_i64, _vp, _c_int, _vp, _c_i64, _c_i64, _c_int, _vp, _vp, _vp,
+                                  _vp, _vp, _vp]),
+    "gcnb_copy_d2h": (_c_int, [_vp, _vp, ctypes.c_size_t]),
 }
 
 

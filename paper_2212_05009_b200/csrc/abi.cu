@@ -135,6 +135,13 @@ extern "C" int gcnb_device_count(int* out) {
   return GCNB_OK;
 }
 
+extern "C" int gcnb_copy_d2h(void* dst_host, const void* src_dev, size_t bytes) {
+  GCNB_REQUIRE(dst_host && src_dev, "copy d2h: null pointer");
+  cudaError_t e = cudaMemcpy(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "copy d2h");
+  return GCNB_OK;
+}
+
 extern "C" int gcnb_malloc(void** dptr, size_t bytes) {
   GCNB_REQUIRE(dptr != nullptr, "malloc: null output");
   cudaError_t e = cudaMalloc(dptr, bytes ? bytes : 16);

@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(AW_THREADS, 1)
       e[j] = (k < SE && k < nn) ? ldg_int2(er + k) : make_int2(0, 0);
     }
     for (int base = 0; base < maxnn; base += SE) {
-      int2* buf = wst + ((base / SE) & 1) * GPW * (SE + 1) + g * (SE + 1);
+      // idle lanes (g == GPW when 32 % G != 0) address group GPW - 1's slots (never stored)
+      int2* buf = wst + ((base / SE) & 1) * GPW * (SE + 1) + min(g, GPW - 1) * (SE + 1);
 #pragma unroll
       for (int j = 0; j < JE; ++j) {
         const int k = j * G + gl;

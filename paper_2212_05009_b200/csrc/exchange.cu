@@ -97,6 +97,50 @@ __global__ void k_wait(const unsigned long long* flags, WaitArgs a, unsigned lon
   }
 }
 
+// Halo pack fused into a producing kernel's epilogue (north_star subsystem 2):
+// row r of the output, as it is stored, is also stored into every receiver's
+// halo slot that the plan assigns to it (map[map_ptr[r] .. map_ptr[r+1]) =
+// {segment, position}; segment s is receiver s's halo block for this rank, a
+// peer-mapped NVLink address), and once every block's stores are visible the
+// last block rings the receivers' doorbells — the k_pack protocol without the
+// separate launch and without re-reading the rows.
+struct EpiPack {
+  float4* dst[GCNB_MAX_PEERS];
+  unsigned long long* flag[GCNB_MAX_PEERS];
+  const int* map_ptr;
+  const int2* map;
+  int* counter;
+  int n_seg;
+  int ldd4;
+};
+
+__device__ __forceinline__ void epi_store(const EpiPack& pk, int row, int ch, float4 v) {
+  if (!pk.map_ptr) return;
+  const int e1 = __ldg(pk.map_ptr + row + 1);
+  for (int e = __ldg(pk.map_ptr + row); e < e1; ++e) {
+    const int2 m = __ldg(pk.map + e);
+    pk.dst[m.x][(size_t)m.y * pk.ldd4 + ch] = v;
+  }
+}
+
+// All threads of the block call this at the end of the kernel.
+__device__ __forceinline__ void epi_signal(const EpiPack& pk) {
+  if (!pk.map_ptr) return;
+  __syncthreads();
+  __shared__ int last;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    last = (atomicAdd(pk.counter, 1) == (int)gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence_system();
+    *pk.counter = 0;
+    for (int s = 0; s < pk.n_seg; ++s)
+      if (pk.flag[s]) red_release_sys_add(pk.flag[s], 1ull);
+  }
+}
+
 // label[r] >= 0 marks a labelled own row.
 constexpr int LOSS_BLOCKS_MAX = 148 * 8;
 
@@ -110,7 +154,7 @@ __device__ __forceinline__ float f4get(const float4& v, int e) {
 template <int LPR, int VPL>
 __global__ void __launch_bounds__(NT) k_loss(const float4* __restrict__ H4, int ldh4, int n_rows, int d,
                                              const int* __restrict__ label, double inv_n, float4* __restrict__ G4,
-                                             int ldg4, int act, double* __restrict__ partials) {
+                                             int ldg4, int act, double* __restrict__ partials, const EpiPack pk) {
   constexpr int GPW = 32 / LPR;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -128,7 +172,10 @@ __global__ void __launch_bounds__(NT) k_loss(const float4* __restrict__ H4, int 
     y_next = row + stride < n_rows ? __ldg(label + row + stride) : -1;
     if (!__any_sync(0xffffffffu, y >= 0)) {  // no labelled row in this warp (warp-uniform): zeros only
       if (row < n_rows)
-        for (int ch = gl; ch < ldg4; ch += LPR) G4[(size_t)row * ldg4 + ch] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int ch = gl; ch < ldg4; ch += LPR) {
+          G4[(size_t)row * ldg4 + ch] = make_float4(0.f, 0.f, 0.f, 0.f);
+          epi_store(pk, row, ch, make_float4(0.f, 0.f, 0.f, 0.f));
+        }
       continue;
     }
     float4 hv[VPL];
@@ -161,7 +208,10 @@ __global__ void __launch_bounds__(NT) k_loss(const float4* __restrict__ H4, int 
     if (row >= n_rows) continue;
     float4* g = G4 + (size_t)row * ldg4;
     if (y < 0) {
-      for (int ch = gl; ch < ldg4; ch += LPR) g[ch] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int ch = gl; ch < ldg4; ch += LPR) {
+        g[ch] = make_float4(0.f, 0.f, 0.f, 0.f);
+        epi_store(pk, row, ch, make_float4(0.f, 0.f, 0.f, 0.f));
+      }
       continue;
     }
     const float lse = logf(s);
@@ -182,8 +232,12 @@ __global__ void __launch_bounds__(NT) k_loss(const float4* __restrict__ H4, int 
         }
       }
       g[ch] = make_float4(o[0], o[1], o[2], o[3]);
+      epi_store(pk, row, ch, make_float4(o[0], o[1], o[2], o[3]));
     }
-    for (int ch = gl + VPL * LPR; ch < ldg4; ch += LPR) g[ch] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int ch = gl + VPL * LPR; ch < ldg4; ch += LPR) {
+      g[ch] = make_float4(0.f, 0.f, 0.f, 0.f);
+      epi_store(pk, row, ch, make_float4(0.f, 0.f, 0.f, 0.f));
+    }
   }
   // fixed-order block reduction of the per-lane NLL sums
 #pragma unroll
@@ -196,6 +250,7 @@ __global__ void __launch_bounds__(NT) k_loss(const float4* __restrict__ H4, int 
     for (int w = 0; w < WARPS; ++w) t += wsum[w];
     partials[blockIdx.x] = t;
   }
+  epi_signal(pk);
 }
 
 // One warp: lane-strided partial sums, then a fixed xor tree (deterministic).
@@ -353,9 +408,49 @@ extern "C" int gcnb_wait_flags(const uint64_t* flags, const int32_t* srcs_host, 
 
 extern "C" int gcnb_loss_scratch_doubles(void) { return LOSS_BLOCKS_MAX; }
 
+namespace {
+int loss_grad(const float* h, int32_t ldh, int32_t n_rows, int32_t d, const int32_t* label, double inv_n_labeled,
+              float* g, int32_t ldg, int32_t act, double* scratch, double* loss_sum, cudaStream_t st,
+              const EpiPack& pk);
+}  // namespace
+
 extern "C" int gcnb_loss_grad_f32(const float* h, int32_t ldh, int32_t n_rows, int32_t d, const int32_t* label,
                                   double inv_n_labeled, float* g, int32_t ldg, int32_t act, double* scratch,
                                   double* loss_sum, void* stream) {
+  EpiPack pk{};
+  return loss_grad(h, ldh, n_rows, d, label, inv_n_labeled, g, ldg, act, scratch, loss_sum, (cudaStream_t)stream,
+                   pk);
+}
+
+extern "C" int gcnb_loss_grad_pack_f32(const float* h, int32_t ldh, int32_t n_rows, int32_t d, const int32_t* label,
+                                       double inv_n_labeled, float* g, int32_t ldg, int32_t act, double* scratch,
+                                       double* loss_sum, const int32_t* map_ptr, const int32_t* map,
+                                       float* const* dst, uint64_t* const* flags, int32_t n_seg, int32_t ldd,
+                                       int32_t* counter, void* stream) {
+  GCNB_REQUIRE(n_seg >= 0 && n_seg <= GCNB_MAX_PEERS, "loss pack: n_seg=%d out of range", n_seg);
+  GCNB_REQUIRE(n_seg == 0 || (map_ptr && map && dst && flags && counter && ldd % 4 == 0 && ldd >= ldg),
+               "loss pack: null or inconsistent pack arguments");
+  EpiPack pk{};
+  if (n_seg > 0) {
+    pk.map_ptr = map_ptr;
+    pk.map = reinterpret_cast<const int2*>(map);
+    pk.counter = counter;
+    pk.n_seg = n_seg;
+    pk.ldd4 = ldd / 4;
+    for (int s = 0; s < n_seg; ++s) {
+      GCNB_REQUIRE(dst[s] && aligned16(dst[s]), "loss pack: destination %d invalid", s);
+      pk.dst[s] = reinterpret_cast<float4*>(dst[s]);
+      pk.flag[s] = reinterpret_cast<unsigned long long*>(flags ? flags[s] : nullptr);
+    }
+  }
+  return loss_grad(h, ldh, n_rows, d, label, inv_n_labeled, g, ldg, act, scratch, loss_sum, (cudaStream_t)stream,
+                   pk);
+}
+
+namespace {
+int loss_grad(const float* h, int32_t ldh, int32_t n_rows, int32_t d, const int32_t* label, double inv_n_labeled,
+              float* g, int32_t ldg, int32_t act, double* scratch, double* loss_sum, cudaStream_t st,
+              const EpiPack& pk) {
   GCNB_REQUIRE(n_rows >= 0 && d >= 1 && ldh >= d && ldg >= d, "loss: bad shapes");
   GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "loss: unknown activation %d", act);
   GCNB_REQUIRE(scratch && loss_sum, "loss: scratch and loss_sum required");
@@ -363,7 +458,6 @@ extern "C" int gcnb_loss_grad_f32(const float* h, int32_t ldh, int32_t n_rows, i
   GCNB_REQUIRE(d <= 256, "loss: class count %d above 256", d);
   GCNB_REQUIRE(ldh % 4 == 0 && ldg % 4 == 0 && (n_rows == 0 || (aligned16(h) && aligned16(g))),
                "loss: row strides must be multiples of 4 floats and operands 16-byte aligned");
-  cudaStream_t st = (cudaStream_t)stream;
   const int c4 = (d + 3) / 4;
   int lpr = 1;
   while (lpr < 32 && lpr < c4) lpr <<= 1;
@@ -371,18 +465,20 @@ extern "C" int gcnb_loss_grad_f32(const float* h, int32_t ldh, int32_t n_rows, i
   const int rows_per_block = NT / lpr;
   const int grid = std::max(1, std::min((n_rows + rows_per_block - 1) / rows_per_block, LOSS_BLOCKS_MAX));
   if (n_rows > 0) {
-    using LossFn = void (*)(const float4*, int, int, int, const int*, double, float4*, int, int, double*);
+    using LossFn = void (*)(const float4*, int, int, int, const int*, double, float4*, int, int, double*,
+                            const EpiPack);
     LossFn fn = vpl == 2 ? k_loss<32, 2>
               : lpr == 1 ? k_loss<1, 1> : lpr == 2 ? k_loss<2, 1> : lpr == 4 ? k_loss<4, 1>
               : lpr == 8 ? k_loss<8, 1> : lpr == 16 ? k_loss<16, 1> : k_loss<32, 1>;
     fn<<<grid, NT, 0, st>>>(reinterpret_cast<const float4*>(h), ldh / 4, n_rows, d, label, inv_n_labeled,
-                            reinterpret_cast<float4*>(g), ldg / 4, act, scratch);
-    GCNB_AFTER_LAUNCH("loss grad");
+                            reinterpret_cast<float4*>(g), ldg / 4, act, scratch, pk);
+    GCNB_AFTER_LAUNCH(pk.map_ptr ? "loss grad (+ fused halo pack)" : "loss grad");
   }
   k_sum_partials_f64<<<1, 32, 0, st>>>(scratch, n_rows > 0 ? grid : 0, loss_sum);
   GCNB_AFTER_LAUNCH("loss sum");
   return GCNB_OK;
 }
+}  // namespace
 
 extern "C" int gcnb_push_f32(const float* src, int64_t n, float* const* dst, uint64_t* const* flags, int32_t n_dst,
                              int32_t* counter, void* stream) {

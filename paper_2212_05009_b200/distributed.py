@@ -293,6 +293,12 @@ class DistributedTrainer:
         self.ar_flag = [self.peer_base[r] + infos[r]["off"]["flags_ar"] + 8 * me for r in range(p)]
         self.ar_srcs = [r for r in range(p) if r != me]
         self.bar_flag = [self.peer_base[r] + infos[r]["off"]["flags_bar"] + 8 * me for r in range(p) if r != me]
+        # halo packs run on their own stream, concurrent with the interior
+        # aggregation of the compute stream (joined back once per epoch)
+        self.comm_stream = torch.cuda.Stream(device)
+        # fuse the halo pack into producing kernels where one exists (the loss
+        # kernel for the last layer's backward exchange); GCNB_FUSE_PACK=0: separate k_pack
+        self.fuse_pack = os.environ.get("GCNB_FUSE_PACK", "1") != "0"
         torch.cuda.synchronize(device)
         dist.barrier()
         self.graphs = {}
@@ -307,13 +313,33 @@ class DistributedTrainer:
             _lib.call("gcnb_wait_flags", flags.data_ptr(), _lib.int_array(srcs), len(srcs), expected.data_ptr(),
                       self.err.data_ptr(), self.timeout_ms, self.st.stream())
 
+    def _pack(self, phase: str, k: int) -> None:
+        """Pack this rank's plan rows of the layer-k operand into the peers'
+        halos (NVLink stores + doorbells) on the comm stream, once the producer
+        of the operand (on the compute stream) has finished; the compute stream
+        goes on with the interior rows meanwhile."""
+        import torch
+
+        cur = torch.cuda.current_stream(self.device)
+        self.comm_stream.wait_stream(cur)
+        with torch.cuda.stream(self.comm_stream):
+            # the packs' last-block counter (counter[2]) is not the allreduce
+            # push's (counter[0]): a pack can still run when the push starts
+            cnt = self.counter.data_ptr() + 8
+            if phase == "fwd":
+                self.st.pack_to("fwd", k, self.fwd_bases[k], flags=self.halo_flag_fwd, counter=cnt)
+            else:
+                self.st.pack_to("bwd", k, self.bwd_bases[k], flags=self.halo_flag_bwd, counter=cnt)
+
     def enqueue_epoch(self, parity: int, comm: bool = True) -> None:
+        import torch
+
         st, L = self.st, self.st.n_layers
         cnt = self.counter.data_ptr()
         for k in range(1, L + 1):
             st.fwd_transform(k)
             if comm:
-                st.pack_to("fwd", k, self.fwd_bases[k], flags=self.halo_flag_fwd, counter=cnt)
+                self._pack("fwd", k)
             if self.overlap:
                 st.fwd_compute(k, "interior")
             if comm:
@@ -321,13 +347,18 @@ class DistributedTrainer:
             st.fwd_compute(k, "boundary" if self.overlap else "all")
             if self.overlap:
                 st.fwd_finish(k)
-        st.loss_grad(1.0 / self.n_lab)
+        # the backward halo of layer L is packed by the loss kernel itself
+        fused_L = comm and self.fuse_pack and not st.skips_bwd_exchange(L) and bool(st.layout.bwd.send_dst)
+        if fused_L:
+            st.loss_grad(1.0 / self.n_lab, pack=(self.bwd_bases[L], self.halo_flag_bwd, self.counter.data_ptr() + 12))
+        else:
+            st.loss_grad(1.0 / self.n_lab)
         for k in range(L, 0, -1):
             if st.skips_bwd_exchange(k):
                 st.reduce_dw(k, st.dw_from_forward(k))
                 continue
-            if comm:
-                st.pack_to("bwd", k, self.bwd_bases[k], flags=self.halo_flag_bwd, counter=cnt)
+            if comm and not (k == L and fused_L):
+                self._pack("bwd", k)
             if self.overlap:
                 gi = st.bwd_compute(k, "interior", slot=0)
                 if comm:
@@ -360,6 +391,8 @@ class DistributedTrainer:
                       float(st.learning_rate), st.stream())
         for k in range(1, L + 1):
             st.dw_total[k] = st.dw_sum[k]
+        # every pack of this epoch has read its operand before the next epoch writes it
+        torch.cuda.current_stream(self.device).wait_stream(self.comm_stream)
         st._has_trace = st._has_grad = True
 
     def device_barrier(self) -> None:

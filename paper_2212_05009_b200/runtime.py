@@ -558,15 +558,49 @@ class ProcState:
                       None, n, self.partials[k].data_ptr(), self.stream())
         return used
 
-    def loss_grad(self, inv_n_labeled: float) -> None:
-        """runtime._local_loss_grad: loss_sum and G^L for own rows."""
+    def send_map(self, phase: str):
+        """Row-major inverse of the phase's send lists, for halo packs fused into
+        a producer's epilogue: (map_ptr [n_own+1], map [R, 2] = {segment,
+        position}) on the device, segments in layout send_dst order."""
+        key = f"_smap_{phase}"
+        if not hasattr(self, key):
+            lay = self.layout.fwd if phase == "fwd" else self.layout.bwd
+            idx = np.asarray(lay.send_idx, dtype=np.int64)
+            seg = np.repeat(np.arange(len(lay.send_dst), dtype=np.int64), np.diff(lay.send_ptr))
+            pos = np.arange(len(idx), dtype=np.int64) - np.asarray(lay.send_ptr, dtype=np.int64)[seg]
+            order = np.argsort(idx, kind="stable")
+            ptr = np.zeros(self.n_own + 1, dtype=np.int64)
+            np.cumsum(np.bincount(idx, minlength=self.n_own), out=ptr[1:])
+            m = np.stack([seg[order], pos[order]], axis=1).astype(np.int32)
+            with torch.cuda.device(self.device):
+                setattr(self, key, (torch.from_numpy(ptr.astype(np.int32)).to(self.device),
+                                    torch.from_numpy(m if len(m) else np.zeros((1, 2), np.int32)).to(self.device)))
+        return getattr(self, key)
+
+    def loss_grad(self, inv_n_labeled: float, pack=None) -> None:
+        """runtime._local_loss_grad: loss_sum and G^L for own rows.  pack =
+        (dst_bases, flags, counter) fuses the backward halo pack of layer L into
+        the loss kernel (G^L rows stored into the receivers' halos as computed)."""
         L = self.n_layers
         h, g = self.hbuf[L], self.gext[L]
         d = self.dims[L]
-        with span("loss", 4 * self.n_own + 4 * d * (self.n_labeled + self.n_own), 0, self.stream()):
-            _lib.call("gcnb_loss_grad_f32", h.data_ptr(), h.shape[1], self.n_own, d, self.label.data_ptr(),
-                      float(inv_n_labeled), g.data_ptr(), g.shape[1], self.act, self.loss_scratch.data_ptr(),
-                      self.loss_sum.data_ptr(), self.stream())
+        if pack is None:
+            with span("loss", 4 * self.n_own + 4 * d * (self.n_labeled + self.n_own), 0, self.stream()):
+                _lib.call("gcnb_loss_grad_f32", h.data_ptr(), h.shape[1], self.n_own, d, self.label.data_ptr(),
+                          float(inv_n_labeled), g.data_ptr(), g.shape[1], self.act, self.loss_scratch.data_ptr(),
+                          self.loss_sum.data_ptr(), self.stream())
+            return
+        dst_bases, flags, counter = pack
+        lay = self.layout.bwd
+        ld = g.shape[1]
+        dsts = [dst_bases[dst][0] + (dst_bases[dst][1] + slot) * ld * 4 for dst, slot in zip(lay.send_dst, lay.dst_slot)]
+        mp, mm = self.send_map("bwd")
+        r = int(lay.send_ptr[-1])
+        with span("loss", 4 * self.n_own + 4 * d * (self.n_labeled + self.n_own) + 4 * ld * r, 0, self.stream()):
+            _lib.call("gcnb_loss_grad_pack_f32", h.data_ptr(), h.shape[1], self.n_own, d, self.label.data_ptr(),
+                      float(inv_n_labeled), g.data_ptr(), ld, self.act, self.loss_scratch.data_ptr(),
+                      self.loss_sum.data_ptr(), mp.data_ptr(), mm.data_ptr(), _lib.ptr_array(dsts),
+                      _lib.ptr_array(flags), len(dsts), ld, counter, self.stream())
 
     def bwd_compute(self, k: int, rows: str = "all", slot: int = 0) -> int:
         """runtime._bwd_compute: G^{k-1} (k > 1) and ΔW^k partials; returns slots used."""

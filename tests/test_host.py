@@ -242,3 +242,34 @@ class TestNormalizeFastPath:
         a = gb.CsrMatrix(4, 4, [0, 0, 1, 1, 1], [3], [2.0])
         t = gb.normalize_adjacency(a)
         assert t.has_full_diagonal() and t.nnz == 5
+
+
+def test_compat_install_rebinds_reference_names():
+    """compat.install() rebinds gcnpart's runtime names in gcnpart.runtime,
+    the package namespace and gcnpart.cli; uninstall() restores them."""
+    import importlib
+    import sys
+    from pathlib import Path
+
+    for p in (Path(__file__).resolve().parents[1] / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (p / "gcnpart").exists():
+            sys.path.insert(0, str(p))
+            break
+    else:
+        pytest.skip("gcnpart not importable here")
+    gcnpart = importlib.import_module("gcnpart")
+    from paper_2212_05009_b200 import compat, runtime
+
+    orig = gcnpart.scatter
+    compat.install(gcnpart)
+    try:
+        import gcnpart.cli as cli
+
+        for mod in (gcnpart, gcnpart.runtime, cli):
+            assert mod.scatter is runtime.scatter
+            assert mod.train_epochs is runtime.train_epochs
+        assert gcnpart.SimNetwork is runtime.DeviceNetwork
+        assert gcnpart.CommError is runtime.CommError
+    finally:
+        compat.uninstall(gcnpart)
+    assert gcnpart.scatter is orig
