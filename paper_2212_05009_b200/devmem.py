@@ -52,8 +52,11 @@ def stream_handle(stream, dev) -> int:
 
 
 def empty_rows(n: int, d: int, dev, ld: int | None = None) -> torch.Tensor:
-    """Zero-filled (n, ld) fp32 block (zero pads are an invariant of the path)."""
-    return torch.zeros((max(int(n), 0), ld_of(d) if ld is None else ld), dtype=torch.float32, device=dev)
+    """Zero-filled (n, ld) fp32 block (zero pads are an invariant of the path).
+    A rank that owns no rows (a mini-batch can leave one empty) still gets a
+    valid, aligned pointer: the (0, ld) view of a one-row allocation."""
+    ld = ld_of(d) if ld is None else ld
+    return torch.zeros((max(int(n), 1), ld), dtype=torch.float32, device=dev)[: max(int(n), 0)]
 
 
 def upload_dense(h: np.ndarray, dev, ld: int | None = None) -> torch.Tensor:

@@ -386,6 +386,7 @@ class DistributedTrainer:
         else:
             _lib.call("gcnb_sum_slots_f32", st.dwpack.data_ptr(), 1, self.slot, st.n_pack, st.dwsum_pack.data_ptr(),
                       self.loss_total.data_ptr(), st.stream())
+        st.mark_weights_updated()
         with span("sgd", 12 * st.n_pack, 2 * st.n_pack, st.stream()):
             _lib.call("gcnb_sgd_f32", st.wpack.data_ptr(), st.dwsum_pack.data_ptr(), st.n_pack,
                       float(st.learning_rate), st.stream())

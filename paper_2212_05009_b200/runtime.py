@@ -323,6 +323,7 @@ class ProcState:
             self.dwpack = torch.zeros(self.n_pack + 4, dtype=torch.float32, device=dev)
             self.dwsum_pack = torch.zeros(self.n_pack + 4, dtype=torch.float32, device=dev)
             self.w, self.dw, self.dw_sum = views(self.wpack), views(self.dwpack), views(self.dwsum_pack)
+            self._w_host = [np.zeros((self.dims[k - 1], self.dims[k])) for k in range(1, L + 1)]
             for k in range(1, L + 1):
                 self._upload_weight(k - 1, model.weights[k - 1])
             self.dw_total = [None] * (L + 1)  # allreduced ΔW of the last backward sweep
@@ -397,8 +398,19 @@ class ProcState:
 
     @property
     def weights(self) -> list:
-        ws = [devmem.download(self.w[k], self.dims[k - 1], self.dims[k]) for k in range(1, self.n_layers + 1)]
+        """Host copies of W^1..W^L.  Until a training step changes them on the
+        device, the exact fp64 arrays last uploaded (a replica no epoch has
+        touched equals its source bit for bit, as in the reference, runtime.py:271);
+        afterwards the device's fp32 weights."""
+        if self._w_host is not None:
+            ws = [w.copy() for w in self._w_host]
+        else:
+            ws = [devmem.download(self.w[k], self.dims[k - 1], self.dims[k]) for k in range(1, self.n_layers + 1)]
         return _WeightList(self, ws)
+
+    def mark_weights_updated(self) -> None:
+        """A step changed the device weights: host views download them from now on."""
+        self._w_host = None
 
     @weights.setter
     def weights(self, ws) -> None:
@@ -410,6 +422,10 @@ class ProcState:
         if w.shape != (self.dims[k], self.dims[k + 1]):
             raise ValueError(f"W^{k + 1} has shape {w.shape}, expected {(self.dims[k], self.dims[k + 1])}")
         self.w[k + 1][:, : self.dims[k + 1]].copy_(torch.from_numpy(w.astype(np.float32)))
+        if self._w_host is None:  # other layers come from the device from now on
+            self._w_host = [devmem.download(self.w[j], self.dims[j - 1], self.dims[j]).astype(np.float64)
+                            for j in range(1, self.n_layers + 1)]
+        self._w_host[k] = np.array(w, dtype=np.float64)
 
     @property
     def a_fwd_local(self):
@@ -609,6 +625,10 @@ class ProcState:
         gi, gb, ga = self.bwd_grids[k]
         used = {"all": ga, "interior": gi, "boundary": gb}[rows]
         g = self.gext[k]
+        if n_sel == 0:  # no rows here (e.g. a mini-batch left this rank empty): zero ΔW contribution
+            part = self.partials[k][slot:slot + used]
+            _lib.call("gcnb_memset_async", part.data_ptr(), 0, part.numel() * 4, self.stream())
+            return used
         if self.bwd_split(k):
             # aggregation alone (span bwd{k}); the dense epilogue (G^{k-1}, ΔW^k
             # partials) runs over all own rows in bwd_finish — right away for
@@ -665,6 +685,8 @@ class ProcState:
 
     def reduce_dw(self, k: int, n_slots: int, apply_sgd: bool = False) -> None:
         """ΔW^k = Σ of the layer's block partials (fixed order); optionally fused with SGD."""
+        if apply_sgd:
+            self.mark_weights_updated()
         size = self.dw[k].numel()
         algo = 4 * size * (n_slots + 1) + (8 * size if apply_sgd else 0)
         with span(f"reduce{k}", algo, size * n_slots, self.stream()):
@@ -672,6 +694,7 @@ class ProcState:
                       self.w[k].data_ptr() if apply_sgd else None, float(self.learning_rate), self.stream())
 
     def sgd(self, k: int, dw: torch.Tensor) -> None:
+        self.mark_weights_updated()
         size = self.w[k].numel()
         with span(f"sgd{k}", 12 * size, 2 * size, self.stream()):
             _lib.call("gcnb_sgd_f32", self.w[k].data_ptr(), dw.data_ptr(), size, float(self.learning_rate),
@@ -1007,9 +1030,12 @@ def _train_minibatch(states, net, labels, epochs: int, mode, dev) -> list:
             slot = torch.zeros(1, dtype=torch.float64, device=dev)
             _run_step(sub_states, net, eff, n_lab, e, step, slot)
             losses.append(float(slot.item()) / n_lab if n_lab else 0.0)
+            if n_lab == 0:
+                continue  # no labelled vertex in the batch: ΔW = 0, the weights stay exactly as they were
             for st, sub in zip(states, sub_states):
                 for k in range(1, st.n_layers + 1):
                     st.w[k].copy_(sub.w[k])
+                st.mark_weights_updated()
         ev1.record()
         ev1.synchronize()
         wall = ev0.elapsed_time(ev1) / 1e3
