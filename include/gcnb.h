@@ -301,6 +301,21 @@ int gcnb_layout_fill(const int64_t* rp, const int64_t* ci, const double* val, in
                      int32_t n_own, const uint64_t* keys, int64_t halo_k0, int64_t n_halo, int32_t sort_rows,
                      int64_t* row_ptr_out, int32_t* ext_col_out, double* val_out, int32_t* has_halo_out,
                      int32_t* colmap_scratch, void* stream);
+/* ---- setup: graph ingest on the device, bit-exact with numpy -
+ * gcnb_normalize_f64  = sparse.normalize_adjacency(a, add_self_loops=True)
+ *   (sparse.py:167-193); two passes: out_ci == NULL sizes out_rp / *nnz_out;
+ * gcnb_transpose_f64  = sparse.transpose_sparse (sparse.py:226-234);
+ * gcnb_induced_pattern = models.induced_pattern(a, batch, add_diagonal=False)
+ *   (models.py:254-276), batch sorted; two passes like normalize;
+ *   pos_scratch: n int64 set to -1 by the caller.  All synchronise `stream`. */
+int gcnb_normalize_f64(const int64_t* rp, const int64_t* ci, const double* val, int64_t n, int64_t* out_rp,
+                       int64_t* out_ci, double* out_val, int64_t* nnz_out, void* stream);
+int gcnb_transpose_f64(const int64_t* rp, const int64_t* ci, const double* val, int64_t n_rows, int64_t n_cols,
+                       int64_t* out_rp, int64_t* out_ci, double* out_val, void* stream);
+int gcnb_induced_pattern(const int64_t* rp, const int64_t* ci, int64_t n, const int64_t* batch, int64_t B,
+                         int64_t* pos_scratch, int64_t* out_rp, int64_t* out_ci, double* out_val, int64_t* nnz_out,
+                         void* stream);
+
 /* synchronous device -> host copy (library-allocated buffers) */
 int gcnb_copy_d2h(void* dst_host, const void* src_dev, size_t bytes);
 

@@ -88,6 +88,10 @@ _SIGNATURES = {
     "gcnb_layout_fill": (_c_int, [_vp, _vp, _vp, _c_i64, _vp, _c_int, _vp, _c_i64, _c_i64, _c_int, _vp, _vp, _vp,
                                   _vp, _vp, _vp]),
     "gcnb_copy_d2h": (_c_int, [_vp, _vp, ctypes.c_size_t]),
+    "gcnb_normalize_f64": (_c_int, [_vp, _vp, _vp, _c_i64, _vp, _vp, _vp, ctypes.POINTER(_c_i64), _vp]),
+    "gcnb_transpose_f64": (_c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _vp, _vp, _vp, _vp]),
+    "gcnb_induced_pattern": (_c_int, [_vp, _vp, _c_i64, _vp, _c_i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_c_i64),
+                                      _vp]),
 }
 
 

@@ -129,8 +129,18 @@ class RankSchedule:
         return cnt
 
 
-def build_rank(a_hat, owner, p: int, rank: int, directed: bool, row_labels=None):
-    """Global plans + this rank's layout (every rank computes the same plans)."""
+def build_rank(a_hat, owner, p: int, rank: int, directed: bool, row_labels=None, device=None):
+    """Global plans + this rank's layout (every rank computes the same plans),
+    on the GPU for large operators (devplan.py; identical to the host builders)."""
+    from .runtime import _use_device_builder
+
+    if device is not None and _use_device_builder(a_hat, None):
+        from .devplan import build_layouts_device
+
+        a_bwd = transpose_sparse(a_hat) if directed else a_hat
+        plan_fwd, plan_bwd, lays = build_layouts_device(a_hat, a_bwd, np.asarray(owner), p, [rank],
+                                                        row_labels=row_labels, device=device)
+        return plan_fwd, plan_bwd, lays[rank]
     plan_fwd = build_comm_plan(a_hat, owner, p)
     if directed:
         a_bwd = transpose_sparse(a_hat)
@@ -232,7 +242,8 @@ class DistributedTrainer:
         self.p = p
         self.device = device
         self.timeout_ms = timeout_ms
-        plan_fwd, plan_bwd, layout = build_rank(a_hat, owner, p, self.rank, directed, row_labels)
+        torch.cuda.set_device(device)
+        plan_fwd, plan_bwd, layout = build_rank(a_hat, owner, p, self.rank, directed, row_labels, device=device)
         self.layout = layout
         self.sched = RankSchedule(plan_fwd, plan_bwd, self.rank, len(model.dims) - 1)
         dims = tuple(int(d) for d in model.dims)
@@ -299,6 +310,8 @@ class DistributedTrainer:
         # fuse the halo pack into producing kernels where one exists (the loss
         # kernel for the last layer's backward exchange); GCNB_FUSE_PACK=0: separate k_pack
         self.fuse_pack = os.environ.get("GCNB_FUSE_PACK", "1") != "0"
+        if self.fuse_pack:
+            self.st.send_map("bwd")  # device arrays built now, never inside a graph capture
         torch.cuda.synchronize(device)
         dist.barrier()
         self.graphs = {}
@@ -321,7 +334,10 @@ class DistributedTrainer:
         import torch
 
         cur = torch.cuda.current_stream(self.device)
-        self.comm_stream.wait_stream(cur)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        self.comm_stream.wait_event(ev)
+        self._forked = True
         with torch.cuda.stream(self.comm_stream):
             # the packs' last-block counter (counter[2]) is not the allreduce
             # push's (counter[0]): a pack can still run when the push starts
@@ -336,6 +352,7 @@ class DistributedTrainer:
 
         st, L = self.st, self.st.n_layers
         cnt = self.counter.data_ptr()
+        self._forked = False
         for k in range(1, L + 1):
             st.fwd_transform(k)
             if comm:
@@ -393,7 +410,10 @@ class DistributedTrainer:
         for k in range(1, L + 1):
             st.dw_total[k] = st.dw_sum[k]
         # every pack of this epoch has read its operand before the next epoch writes it
-        torch.cuda.current_stream(self.device).wait_stream(self.comm_stream)
+        if self._forked:
+            ev = torch.cuda.Event()
+            ev.record(self.comm_stream)
+            torch.cuda.current_stream(self.device).wait_event(ev)
         st._has_trace = st._has_grad = True
 
     def device_barrier(self) -> None:

@@ -211,15 +211,28 @@ def partition_graph_fm(g, cfg: PartitionConfig) -> Partition:
 def stochastic_net_list(a, batch_size: int, b: int, seed: int) -> NetList:
     """SHP's merged hypergraph (models.py:279-291): the column nets of each of
     b sampled batches' induced patterns (with self loops), pins mapped back to
-    global ids, concatenated batch by batch; full-graph vertex weights."""
+    global ids, concatenated batch by batch; full-graph vertex weights.  Large
+    graphs induce the batches on the GPU (devingest; same patterns)."""
     from .host import MiniBatchSpec, induced_pattern, sample_batches
+    from .sparse import _device_ingest
 
     if a.n_rows != a.n_cols:
         raise ValueError("matrix must be square")
     ptrs, pins = [np.zeros(1, dtype=np.int64)], []
     base = 0
+    g = None
+    if _device_ingest(a):
+        from .devingest import DeviceGraph, induced_pattern_device
+
+        g = DeviceGraph(a)
     for batch in sample_batches(a.n_rows, MiniBatchSpec(batch_size), b, seed):
-        sub = column_net_model(induced_pattern(a, batch))
+        if g is not None:  # induced pattern + full diagonal, as induced_pattern(a, batch) builds it
+            from .sparse import _add_identity
+
+            sub_p = induced_pattern_device(g, batch)
+            sub = column_net_model(_add_identity(sub_p))
+        else:
+            sub = column_net_model(induced_pattern(a, batch))
         pins.append(batch[sub.pins])
         ptrs.append(sub.ptr[1:] + base)
         base += len(sub.pins)
@@ -233,6 +246,52 @@ def partition_stochastic(a, batch_size: int, b: int, cfg: PartitionConfig) -> Pa
     if b < 1:
         raise ValueError("stochastic partitioning needs at least one batch")
     return partition_hypergraph_fm(stochastic_net_list(a, batch_size, b, cfg.seed), cfg)
+
+
+def contract(h: NetList, labels: np.ndarray, weights) -> NetList:
+    """Nets of `h` contracted onto vertex clusters `labels` (0..C-1): each net's
+    pins become its distinct clusters; nets inside one cluster (never cut) are
+    dropped; cluster weight = the sum of its vertices' `weights`."""
+    C = int(labels.max()) + 1
+    net_of = np.repeat(np.arange(h.n_nets, dtype=np.int64), np.diff(h.ptr))
+    key = np.unique(net_of * C + labels[h.pins])
+    net, cl = key // C, key % C
+    cnt = np.bincount(net, minlength=h.n_nets)
+    keep = cnt[net] >= 2
+    net, cl = net[keep], cl[keep]
+    counts = np.bincount(net, minlength=h.n_nets)
+    counts = counts[counts > 0]
+    ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    w = np.bincount(labels, weights=np.asarray(weights, dtype=np.float64), minlength=C).astype(np.int64)
+    return NetList(C, ptr, cl, None, w)
+
+
+def partition_stochastic_ml(a_hat, batch_size: int, b: int, p: int, seed: int = 0, epsilon: float = 0.01,
+                            sweeps: int = 5, fm_passes: int = 8, restarts: int = 3,
+                            labels: np.ndarray | None = None) -> Partition:
+    """Two-level SHP for 10^6-10^8 vertices (the multilevel counterpart of
+    partition_stochastic, as partition_hypergraph_ml is of HP): the merged
+    hypergraph of b sampled batches (stochastic_net_list, rng tag 0xBA7C) is
+    contracted onto label-propagation clusters of the symmetrised pattern, the
+    reference's recursive bisection + FM partitions the coarse hypergraph
+    (rng tag 0x4850), and the assignment is projected back with the k-way
+    weight repair if needed.  Vertex weights are full-graph row counts."""
+    from .locality import community_labels
+
+    weights = np.asarray(a_hat.row_nnz(), dtype=np.int64)
+    if p == 1:
+        return Partition.from_assignment(np.zeros(a_hat.n_rows, dtype=np.int64), weights, 1, epsilon)
+    if labels is None:
+        labels = community_labels(a_hat, sweeps=sweeps)
+    _, lab = np.unique(np.asarray(labels), return_inverse=True)
+    h = stochastic_net_list(a_hat, batch_size, b, seed)
+    cfg = PartitionConfig(p=p, epsilon=epsilon, seed=seed, fm_passes=fm_passes, restarts=restarts)
+    cpi = partition_hypergraph_fm(contract(h, lab, weights), cfg)
+    owner = cpi.assignment[lab]
+    pi = Partition.from_assignment(owner, weights, p, epsilon)
+    if not pi.is_balanced():
+        pi = Partition.from_assignment(_weight_repair(owner, weights, p, epsilon), weights, p, epsilon)
+    return pi
 
 
 def _partition_by_bisection(h: NetList, cfg: PartitionConfig, tag: int) -> Partition:

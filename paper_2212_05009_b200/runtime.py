@@ -736,7 +736,7 @@ class ProcState:
 
 
 def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, device=None,
-            locality: bool = False, reuse_fwd_aggregate: bool = False) -> list:
+            locality: bool = False, reuse_fwd_aggregate: bool = False, builder: str | None = None) -> list:
     """Distribute row blocks per the partition and replicate the weights on the
     device (runtime.py:233-275).  All ranks of this process share `device`.
 
@@ -745,28 +745,49 @@ def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, 
     rows in that order (every host view follows it).
 
     reuse_fwd_aggregate=True computes ΔW¹ from the forward's Â·H⁰ (see
-    ProcState): one aggregation and one halo exchange fewer per epoch."""
+    ProcState): one aggregation and one halo exchange fewer per epoch.
+
+    builder: "device" builds the plan and every rank's layout on the GPU
+    (devplan.py: identical results), "host" with numpy; default: device for
+    operators above DEVICE_BUILDER_MIN_NNZ nonzeros (GCNB_BUILDER overrides)."""
     h0 = dense(h0)
     if h0.shape != (a_hat.n_rows, model.dims[0]):
         raise ValueError(f"h0 has shape {h0.shape}, expected ({a_hat.n_rows}, {model.dims[0]})")
     dev = devmem.device(device)
-    plan_fwd = build_comm_plan(a_hat, pi, p)
-    if directed:
-        a_bwd = transpose_sparse(a_hat)
-        plan_bwd = build_comm_plan(a_bwd, pi, p)
-    else:
-        a_bwd, plan_bwd = a_hat, plan_fwd
+    a_bwd = transpose_sparse(a_hat) if directed else a_hat
     labels = None
     if locality:
         from .locality import locality_keys
 
         labels = locality_keys(a_hat, symmetric=None if directed else True)
-    states = []
-    for m in range(plan_fwd.p):
-        lay = build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, m, row_labels=labels)
-        states.append(ProcState(lay, plan_fwd, plan_bwd, model, h0[lay.global_rows], dev,
-                                reuse_fwd_aggregate=reuse_fwd_aggregate))
-    return states
+    if _use_device_builder(a_hat, builder):
+        from .comm import _owner_and_p
+        from .devplan import build_layouts_device
+
+        owner, p_ = _owner_and_p(pi, p)
+        plan_fwd, plan_bwd, lays = build_layouts_device(a_hat, a_bwd, owner, p_, range(p_), row_labels=labels,
+                                                        device=dev)
+        layouts = [lays[m] for m in range(p_)]
+    else:
+        plan_fwd = build_comm_plan(a_hat, pi, p)
+        plan_bwd = build_comm_plan(a_bwd, pi, p) if directed else plan_fwd
+        layouts = [build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, m, row_labels=labels)
+                   for m in range(plan_fwd.p)]
+    return [ProcState(lay, plan_fwd, plan_bwd, model, h0[lay.global_rows], dev, reuse_fwd_aggregate=reuse_fwd_aggregate)
+            for lay in layouts]
+
+
+# operators with more nonzeros than this build their plan and layouts on the GPU
+DEVICE_BUILDER_MIN_NNZ = 1 << 20
+
+
+def _use_device_builder(a, builder: str | None) -> bool:
+    builder = builder or os.environ.get("GCNB_BUILDER")
+    if builder in ("device", "host"):
+        return builder == "device"
+    if builder is not None:
+        raise ValueError(f"unknown builder {builder!r}")
+    return a.nnz > DEVICE_BUILDER_MIN_NNZ
 
 
 # ---------------------------------------------------------------------------
@@ -1004,6 +1025,27 @@ def _local_labelset(labels, batch: np.ndarray):
     return LabelSet(pos[mine], np.asarray(labels.labels)[mine], labels.n_classes)
 
 
+_DEVICE_GRAPHS: dict = {}
+
+
+def _batch_operator(adjacency, batch: np.ndarray, dev):
+    """Renormalised induced sub-adjacency of a sorted batch (runtime.py:601-602):
+    on the GPU for large graphs (devingest: the adjacency stays resident across
+    steps; bit-identical to the host path), numpy otherwise.  The batch draw
+    itself stays on the host: it is the reference's numpy Generator stream."""
+    if adjacency.nnz >= DEVICE_BUILDER_MIN_NNZ and torch.cuda.is_available():
+        from .devingest import DeviceGraph, induced_pattern_device, normalize_adjacency_device
+
+        key = (id(adjacency), str(dev))
+        g = _DEVICE_GRAPHS.get(key)
+        if g is None or g[0] is not adjacency:
+            g = (adjacency, DeviceGraph(adjacency, dev))
+            _DEVICE_GRAPHS.clear()
+            _DEVICE_GRAPHS[key] = g
+        return normalize_adjacency_device(induced_pattern_device(g[1], batch), dev)
+    return normalize_adjacency(induced_pattern(adjacency, batch, add_diagonal=False), add_self_loops=True)
+
+
 def _train_minibatch(states, net, labels, epochs: int, mode, dev) -> list:
     """Mini-batch branch (runtime.py:593-632): per step a uniform sample
     (rng [seed, 0x7B]), its induced renormalised sub-adjacency, a fresh plan and
@@ -1017,8 +1059,7 @@ def _train_minibatch(states, net, labels, epochs: int, mode, dev) -> list:
         losses = []
         for step in range(mode.batches_per_epoch):
             batch = np.sort(rng.choice(mode.adjacency.n_rows, size=mode.spec.batch_size, replace=False))
-            sub_hat = normalize_adjacency(induced_pattern(mode.adjacency, batch, add_diagonal=False),
-                                          add_self_loops=True)
+            sub_hat = _batch_operator(mode.adjacency, batch, dev)
             st0 = states[0]
             model = GcnModel(st0.dims, tuple(st0.weights), st0.activation, st0.learning_rate)
             sub_states = scatter(sub_hat, np.asarray(mode.features)[batch], np.asarray(mode.owner)[batch], model,

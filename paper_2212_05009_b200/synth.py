@@ -174,6 +174,46 @@ def products(seed: int = 0, n: int = 2_449_029, pairs: int = 61_859_140, blocks:
     return _csr_from_pairs(n, np.concatenate([x, y]), np.concatenate([y, x]))
 
 
+def papers(seed: int = 0, n: int = 1 << 22, out_degree: float = 14.55, blocks: int = 3500, intra: float = 0.8,
+           sigma: float = 1.0, block_offset: float = 16.0) -> RawPattern:
+    """ogbn-papers100M shape at reduced n (BASELINE config[4]; 111 M vertices /
+    1.6 B arcs does not fit this build's host): a DIRECTED degree-corrected SBM
+    with the real graph's mean out-degree 14.55 (1,615,685,872 / 111,059,956),
+    exactly round(n·14.55) distinct arcs, 80 % of them inside the source's block
+    (~1,200 vertices per block, as products), the rest to a block at a
+    two-sided geometric ring offset; log-normal propensities on both ends
+    (citation in- and out-degrees are skewed); relabelled."""
+    rng = np.random.default_rng([seed, 0x9A9E])
+    m = int(round(n * out_degree))
+    block = np.sort(rng.integers(0, blocks, n))
+    bounds = np.searchsorted(block, np.arange(blocks + 1))
+    prop = rng.lognormal(0.0, sigma, n)
+    cum = np.cumsum(prop)
+
+    def inv_cdf(x):
+        return np.minimum(_searchsorted(cum, x), n - 1)
+
+    def draw(k):
+        u = inv_cdf(rng.random(k) * cum[-1])
+        same = rng.random(k) < intra
+        off = rng.geometric(1.0 / block_offset, k) * np.where(rng.random(k) < 0.5, -1, 1)
+        b = np.where(same, block[u], (block[u] + off) % blocks)
+        lo = bounds[b]
+        hi = np.maximum(bounds[b + 1], lo + 1)
+        c_lo = np.where(lo > 0, cum[np.maximum(lo - 1, 0)], 0.0)
+        c_hi = cum[np.minimum(hi, n) - 1]
+        w = inv_cdf(c_lo + rng.random(k) * (c_hi - c_lo))
+        keep = u != w
+        return _uniq(u[keep] * n + w[keep])
+
+    keys = draw(int(m * 1.08))
+    while len(keys) < m:
+        keys = _uniq(np.concatenate([keys, draw(int((m - len(keys)) * 1.5) + 1024)]))
+    keys = _exact_count(keys, m, rng)
+    perm = rng.permutation(n)
+    return _csr_from_pairs(n, perm[keys // n], perm[keys % n])
+
+
 WORKLOADS = {
     # name: (generator, directed, dims)
     "config1": (config1, False, (16, 16, 8)),
@@ -181,4 +221,5 @@ WORKLOADS = {
     "roadnet": (roadnet, False, (16, 16, 8)),
     "products": (products, False, (100, 128, 47)),
     "products3": (products, False, (100, 128, 128, 47)),
+    "papers": (papers, True, (128, 128, 172)),
 }
