@@ -26,14 +26,16 @@ class DeviceGraph:
     def __init__(self, a, dev=None):
         self.dev = dev or torch.device("cuda", torch.cuda.current_device())
         self.n_rows, self.n_cols = int(a.n_rows), int(a.n_cols)
+        self._nnz = int(len(a.col_indices))
         with torch.cuda.device(self.dev):
+            # one padding element keeps the pointers valid for an empty pattern
             self.rp = torch.from_numpy(np.array(a.row_offsets, dtype=np.int64)).to(self.dev)
-            self.ci = torch.from_numpy(np.array(a.col_indices, dtype=np.int64)).to(self.dev)
-            self.val = torch.from_numpy(np.array(a.values, dtype=np.float64)).to(self.dev)
+            self.ci = torch.from_numpy(np.append(np.asarray(a.col_indices, dtype=np.int64), 0)).to(self.dev)
+            self.val = torch.from_numpy(np.append(np.asarray(a.values, dtype=np.float64), 0.0)).to(self.dev)
 
     @property
     def nnz(self) -> int:
-        return int(self.ci.numel())
+        return self._nnz
 
 
 def _host(n_rows, n_cols, rp, ci, val) -> CsrMatrix:

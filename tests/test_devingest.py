@@ -53,6 +53,16 @@ def test_induced_pattern(dev):
     a = _random(2000, 0.004, 7, 0.3, True)
     g = devingest.DeviceGraph(a, dev)
     rng = np.random.default_rng(3)
-    for b in (1, 17, 500, 2000):
+    for b in (1, 2, 17, 500, 2000):
         batch = np.sort(rng.choice(2000, size=b, replace=False))
         _eq(devingest.induced_pattern_device(g, batch), host.induced_pattern(a, batch, add_diagonal=False))
+
+
+def test_empty_pattern(dev):
+    """A batch with no internal edge: the induced pattern is empty, its
+    normalisation is the identity."""
+    a = _random(50, 0.0, 1, 0.0, True)
+    g = devingest.DeviceGraph(a, dev)
+    sub = devingest.induced_pattern_device(g, np.array([3, 9]))
+    _eq(sub, host.induced_pattern(a, np.array([3, 9]), add_diagonal=False))
+    _eq(devingest.normalize_adjacency_device(sub, dev), sparse._normalize_host(sub))
