@@ -183,7 +183,7 @@ WINDOW_ON = os.environ.get("GCNB_AGGWIN", "0") == "1"
 class _DeviceOp:
     """Device copy of one OpLayout."""
 
-    def __init__(self, lay: OpLayout, dev):
+    def __init__(self, lay: OpLayout, dev, window: bool = True):
         self.lay = lay
         self.csr = devmem.upload_csr_arrays(lay.n_own, lay.n_cols, lay.row_ptr, lay.col, lay.val, dev)
         self.interior = devmem.upload_index(lay.interior, dev)
@@ -194,7 +194,7 @@ class _DeviceOp:
                      "boundary": int(lens[lay.boundary].sum())}
         self.dev = dev
         self.win = None  # (nnear, entries) of the windowed aggregation
-        if WINDOW_ON and lay.n_own >= WINDOW_MIN_ROWS:
+        if window and WINDOW_ON and lay.n_own >= WINDOW_MIN_ROWS:
             with torch.cuda.device(dev):
                 self.window()  # built here, never inside a graph capture
 
@@ -235,6 +235,39 @@ class _DeviceOp:
         nnz = self._nnz[rows]
         n_x = self.lay.n_cols if rows == "all" else (self.lay.n_cols * nnz) // max(self._nnz["all"], 1)
         return 4 * (n_sel + 1) + 8 * nnz + 4 * d_in * n_x + 4 * d_out * n_sel
+
+
+class DeviceRows:
+    """Feature rows resident on the GPU (fp32, row stride ld), and the global
+    ids of the rows a rank takes from them: the rank's H⁰ block is gathered on
+    the device by the pack kernel (gcnb_pack_rows_f32 without doorbells) instead
+    of being sliced, converted and uploaded from the host every mini-batch step."""
+
+    def __init__(self, feat: torch.Tensor, d: int, ids=None):
+        self.feat, self.d, self.ids = feat, int(d), ids
+
+    def take(self, ids) -> "DeviceRows":
+        return DeviceRows(self.feat, self.d, np.asarray(ids, dtype=np.int64))
+
+    def gather_into(self, dst: torch.Tensor, d: int, stream) -> None:
+        n = len(self.ids)
+        if n == 0:
+            return
+        idx = torch.from_numpy(self.ids.astype(np.int32)).to(dst.device)
+        ptr = np.array([0, n], dtype=np.int32)
+        _lib.call("gcnb_pack_rows_f32", self.feat.data_ptr(), self.feat.shape[1], d, idx.data_ptr(),
+                  _lib.int_array(ptr), 1, _lib.ptr_array([dst.data_ptr()]), dst.shape[1], None, None, stream)
+        torch.cuda.current_stream(dst.device).synchronize()  # idx is freed on return
+
+    @staticmethod
+    def upload(features, dev) -> "DeviceRows":
+        f = np.asarray(features)
+        d = f.shape[1]
+        t = devmem.empty_rows(f.shape[0], d, dev)
+        chunk = 1 << 18  # bounded host temporaries (fp64 -> fp32 per chunk)
+        for r0 in range(0, f.shape[0], chunk):
+            t[r0:r0 + chunk, :d].copy_(torch.from_numpy(np.ascontiguousarray(f[r0:r0 + chunk], dtype=np.float32)))
+        return DeviceRows(t, d)
 
 
 class _WeightList(list):
@@ -282,7 +315,11 @@ class ProcState:
         self.learning_rate = float(model.learning_rate)
         self.layout = layout
         self.device = dev
-        self._h0_host = np.ascontiguousarray(h0)
+        # h0: host rows of this rank (the reference's st.h0), or a DeviceRows
+        # (features resident on the GPU + this rank's row ids): gathered on the
+        # device, downloaded only if a caller reads st.h0
+        self._h0_dev = h0 if isinstance(h0, DeviceRows) else None
+        self._h0_host = None if self._h0_dev is not None else np.ascontiguousarray(h0)
         self._has_trace = False
         self._has_grad = False
         self.n_labeled = 0
@@ -306,7 +343,10 @@ class ProcState:
                     self.hbuf[k] = self.xext[k + 1][:n]
                 else:
                     self.hbuf[k] = devmem.empty_rows(n, self.dims[k], dev)
-            self.hbuf[0][:, : self.dims[0]].copy_(torch.from_numpy(np.asarray(h0, dtype=np.float32)))
+            if self._h0_dev is not None:
+                self._h0_dev.gather_into(self.hbuf[0], self.dims[0], self.stream())
+            else:
+                self.hbuf[0][:, : self.dims[0]].copy_(torch.from_numpy(np.asarray(h0, dtype=np.float32)))
             self.gext = [None] + [alloc(f"gext{k}", n + R_b, self.dims[k]) for k in range(1, L + 1)]
             # W^1..W^L and ΔW^1..ΔW^L each live in one packed vector, so the ΔW
             # allreduce and the SGD step are single launches; 4 tail floats carry
@@ -373,13 +413,15 @@ class ProcState:
 
     @property
     def h0(self) -> np.ndarray:
+        if self._h0_host is None:
+            self._h0_host = devmem.download(self.hbuf[0], self.n_own, self.dims[0]).astype(np.float64)
         return self._h0_host
 
     @property
     def h(self) -> list:
         if not self._has_trace:
             return []
-        return [devmem.download(self.hbuf[k], self.n_own, self.dims[k]) if k else self._h0_host
+        return [devmem.download(self.hbuf[k], self.n_own, self.dims[k]) if k else self.h0
                 for k in range(self.n_layers + 1)]
 
     @property
@@ -470,7 +512,39 @@ class ProcState:
         self.label.copy_(torch.from_numpy(lab_map))
         self.n_labeled = count
         self._labels_obj = labels
+        self.op_bwd_lab = self._labelled_operator(lab_map, ids)
         return count
+
+    def _labelled_operator(self, lab_map: np.ndarray, labelled_ids: np.ndarray):
+        """The backward operator of the last layer restricted to labelled columns.
+        G^L = grad ⊙ σ′(Z^L) is exactly zero on unlabelled rows (runtime.py:325-332:
+        the NLL gradient only touches labelled rows), so Âᵀ·G^L needs only the
+        labelled columns: the same sums, term for term, without the zero terms
+        (bit-identical: x + 0·v = x).  The halo exchange is unchanged (the
+        reference sends every planned row).  None when it would not pay off."""
+        lay = self.layout.bwd
+        n_own = lay.n_own
+        if lay.nnz < (1 << 16) or n_own == 0:
+            return None
+        colflag = np.zeros(lay.n_cols, dtype=bool)
+        colflag[:n_own] = lab_map[:n_own] >= 0
+        if lay.n_halo:
+            gids = np.concatenate([np.asarray(self.plan_bwd.send[int(src)][self.rank], dtype=np.int64)
+                                   for src in lay.recv_from])
+            srt = np.sort(np.asarray(labelled_ids, dtype=np.int64))
+            pos = np.minimum(np.searchsorted(srt, gids), max(len(srt) - 1, 0))
+            colflag[n_own:] = (srt[pos] == gids) if len(srt) else False
+        keep = colflag[lay.col]
+        if keep.mean() > 0.5:
+            return None
+        rows = np.repeat(np.arange(n_own, dtype=np.int64), np.diff(lay.row_ptr))
+        rp = np.zeros(n_own + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rows[keep], minlength=n_own), out=rp[1:])
+        sub = OpLayout(n_own, lay.n_halo, rp, lay.col[keep], lay.val[keep], lay.interior, lay.boundary,
+                       lay.recv_from, lay.halo_off, lay.halo_len, lay.send_dst, lay.send_ptr, lay.send_idx,
+                       lay.dst_slot)
+        with torch.cuda.device(self.device):
+            return _DeviceOp(sub, self.device, window=False)
 
     def fwd_operand(self, k: int):
         """(tensor, width) that layer k aggregates and exchanges."""
@@ -621,6 +695,8 @@ class ProcState:
     def bwd_compute(self, k: int, rows: str = "all", slot: int = 0) -> int:
         """runtime._bwd_compute: G^{k-1} (k > 1) and ΔW^k partials; returns slots used."""
         op = self.op_bwd
+        if k == self.n_layers and getattr(self, "op_bwd_lab", None) is not None:
+            op = self.op_bwd_lab  # G^L is zero off the labelled rows: only labelled columns
         sel, n_sel = self._rows(op, rows)
         gi, gb, ga = self.bwd_grids[k]
         used = {"all": ga, "interior": gi, "boundary": gb}[rows]
@@ -750,9 +826,13 @@ def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, 
     builder: "device" builds the plan and every rank's layout on the GPU
     (devplan.py: identical results), "host" with numpy; default: device for
     operators above DEVICE_BUILDER_MIN_NNZ nonzeros (GCNB_BUILDER overrides)."""
-    h0 = dense(h0)
-    if h0.shape != (a_hat.n_rows, model.dims[0]):
-        raise ValueError(f"h0 has shape {h0.shape}, expected ({a_hat.n_rows}, {model.dims[0]})")
+    if isinstance(h0, DeviceRows):
+        if h0.ids is not None and len(h0.ids) != a_hat.n_rows or h0.d != model.dims[0]:
+            raise ValueError("device feature rows do not match the operator / model")
+    else:
+        h0 = dense(h0)
+        if h0.shape != (a_hat.n_rows, model.dims[0]):
+            raise ValueError(f"h0 has shape {h0.shape}, expected ({a_hat.n_rows}, {model.dims[0]})")
     dev = devmem.device(device)
     a_bwd = transpose_sparse(a_hat) if directed else a_hat
     labels = None
@@ -773,7 +853,12 @@ def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, 
         plan_bwd = build_comm_plan(a_bwd, pi, p) if directed else plan_fwd
         layouts = [build_rank_layout(a_hat, a_bwd, plan_fwd, plan_bwd, m, row_labels=labels)
                    for m in range(plan_fwd.p)]
-    return [ProcState(lay, plan_fwd, plan_bwd, model, h0[lay.global_rows], dev, reuse_fwd_aggregate=reuse_fwd_aggregate)
+    def rows_of(lay):
+        if isinstance(h0, DeviceRows):  # ids: operator row -> feature row (None: identity)
+            return h0.take(lay.global_rows if h0.ids is None else h0.ids[lay.global_rows])
+        return h0[lay.global_rows]
+
+    return [ProcState(lay, plan_fwd, plan_bwd, model, rows_of(lay), dev, reuse_fwd_aggregate=reuse_fwd_aggregate)
             for lay in layouts]
 
 
@@ -1026,6 +1111,22 @@ def _local_labelset(labels, batch: np.ndarray):
 
 
 _DEVICE_GRAPHS: dict = {}
+_DEVICE_FEATURES: dict = {}
+
+
+def _batch_features(mode, batch: np.ndarray, dev):
+    """H⁰ rows of a batch: for large graphs the full feature matrix stays on the
+    GPU (uploaded once) and each rank gathers its batch rows there; small ones
+    slice on the host, as the reference does (runtime.py:612)."""
+    if mode.adjacency.nnz >= DEVICE_BUILDER_MIN_NNZ and torch.cuda.is_available():
+        key = (id(mode.features), str(dev))
+        f = _DEVICE_FEATURES.get(key)
+        if f is None or f[0] is not mode.features:
+            _DEVICE_FEATURES.clear()
+            f = (mode.features, DeviceRows.upload(mode.features, dev))
+            _DEVICE_FEATURES[key] = f
+        return DeviceRows(f[1].feat, f[1].d, np.asarray(batch, dtype=np.int64))
+    return np.asarray(mode.features)[batch]
 
 
 def _batch_operator(adjacency, batch: np.ndarray, dev):
@@ -1062,8 +1163,9 @@ def _train_minibatch(states, net, labels, epochs: int, mode, dev) -> list:
             sub_hat = _batch_operator(mode.adjacency, batch, dev)
             st0 = states[0]
             model = GcnModel(st0.dims, tuple(st0.weights), st0.activation, st0.learning_rate)
-            sub_states = scatter(sub_hat, np.asarray(mode.features)[batch], np.asarray(mode.owner)[batch], model,
-                                 directed=mode.directed, p=p, device=dev)
+            feats = _batch_features(mode, batch, dev)
+            sub_states = scatter(sub_hat, feats, np.asarray(mode.owner)[batch], model, directed=mode.directed, p=p,
+                                 device=dev)
             sub_labels = _local_labelset(labels, batch)
             n_lab = len(sub_labels) if sub_labels is not None else 0
             eff = sub_labels if sub_labels is not None else LabelSet(np.zeros(0, np.int64), np.zeros(0, np.int64),
