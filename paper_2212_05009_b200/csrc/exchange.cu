@@ -60,6 +60,14 @@ __global__ void __launch_bounds__(NT) k_pack(const float4* __restrict__ X4, int 
   // fence through the barrier (fences are cumulative), so one fence per block
   // suffices; the last block to arrive rings the doorbells.
   __syncthreads();
+  if (gridDim.x == 1) {  // small halo: one block, one fence, no election
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int s = 0; s < a.n_seg; ++s)
+        if (a.seg_ptr[s + 1] > a.seg_ptr[s] && a.flag[s]) red_release_sys_add(a.flag[s], 1ull);
+    }
+    return;
+  }
   __shared__ int last;
   if (threadIdx.x == 0) {
     __threadfence_system();
@@ -380,6 +388,7 @@ extern "C" int gcnb_pack_rows_f32(const float* x, int32_t ldx, int32_t d, const 
   const int c4 = round4(d) / 4;
   const long long work = (long long)total * c4;
   // a few rows per thread: fewer blocks → fewer fences and counter arrivals
+  // (up to 4·NT chunks a single block: one fence, no last-block election)
   const int grid = (int)std::max<long long>(1, std::min<long long>((work + 4 * NT - 1) / (4 * NT), num_sms() * 2));
   k_pack<<<grid, NT, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4*>(x), ldx / 4, c4, idx, a, ld_dst / 4,
                                                 counter, signal);

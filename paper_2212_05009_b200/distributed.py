@@ -261,7 +261,11 @@ class DistributedTrainer:
         self.off = arena_layout(n_own, layout.fwd.n_halo, layout.bwd.n_halo, dims, tf, p, n_pack)
         torch.cuda.set_device(device)
         self.arena = Arena(self.off, device)
-        self.st = ProcState(layout, plan_fwd, plan_bwd, model, np.asarray(h0)[layout.global_rows], device,
+        from .runtime import DeviceRows
+
+        rows_h0 = (h0.take(layout.global_rows if h0.ids is None else h0.ids[layout.global_rows])
+                   if isinstance(h0, DeviceRows) else np.asarray(h0)[layout.global_rows])
+        self.st = ProcState(layout, plan_fwd, plan_bwd, model, rows_h0, device,
                             alloc=self.arena.rows_alloc, reuse_fwd_aggregate=reuse_fwd_aggregate)
         self.sched.skip_bwd1 = self.st.skips_bwd_exchange(1)
         assert self.st.transform_first == tf and self.st.n_pack == n_pack
@@ -668,3 +672,56 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
     tr.close()
     dist.destroy_process_group()
     return line if rank == 0 else None
+
+
+# ---------------------------------------------------------------------------
+# mini-batch training across processes (runtime.py:593-632, one process per GPU)
+
+
+def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int, steps: int, seed: int,
+                    directed: bool, device, timeout_ms: int = 60000):
+    """The reference's mini-batch branch with one process per GPU: every rank
+    draws the same batch (rng [seed, 0x7B], runtime.py:597-600), induces and
+    renormalises it on its device (devingest), builds its own layout of the
+    batch under the fixed owner array (devplan), maps its peers' arenas, runs
+    the step (NVLink halo exchanges + rank-ordered allreduce + SGD, as the
+    full-batch path) and keeps the updated weights for the next step.
+    `features` is a runtime.DeviceRows over the full feature matrix.  Returns
+    (per-step losses, per-step wall seconds, per-step reference words)."""
+    import torch
+    import torch.distributed as dist
+
+    from .host import GcnModel
+    from .runtime import DeviceRows, _batch_operator, _local_labelset
+
+    rng = np.random.default_rng([int(seed), 0x7B])
+    n = raw.n_rows
+    losses, walls, words = [], [], []
+    ws = [np.asarray(w) for w in model.weights]
+    for step in range(steps):
+        torch.cuda.synchronize(device)
+        dist.barrier()
+        t0 = time.perf_counter()
+        batch = np.sort(rng.choice(n, size=spec_batch, replace=False))
+        sub_hat = _batch_operator(raw, batch, device)
+        sub_labels = _local_labelset(labels, batch)
+        if sub_labels is None:  # no labelled vertex: ΔW = 0, weights unchanged (runtime.py:620-625)
+            losses.append(0.0)
+            walls.append(time.perf_counter() - t0)
+            words.append(0)
+            continue
+        m = GcnModel(tuple(model.dims), tuple(ws), model.activation, model.learning_rate)
+        tr = DistributedTrainer(sub_hat, DeviceRows(features.feat, features.d, batch), np.asarray(owner)[batch], p, m,
+                                sub_labels, directed, device, timeout_ms=timeout_ms, overlap=False)
+        tr.enqueue_epoch(0)
+        torch.cuda.synchronize(device)
+        tr.check()
+        losses.append(float(tr.loss_total.item()) / len(sub_labels))
+        ws = [np.asarray(w) for w in tr.st.weights]
+        words.append(reference_words_per_epoch(tr.layout, tuple(model.dims)))
+        dist.barrier()
+        tr.close()        # unmap the peers' arenas ...
+        dist.barrier()    # ... everywhere before any rank frees its own
+        tr.arena.free()
+        walls.append(time.perf_counter() - t0)
+    return losses, walls, words, ws
