@@ -6,7 +6,7 @@ exchanges and the rank-ordered allreduce.  Rank 0 partitions (two-level SHP)
 and broadcasts the owner array; rank 0 prints one JSON line with ms per step,
 words per step and the first step's loss against the fp64 oracle.
 
-    torchrun --nproc-per-node 4 scripts/dist_minibatch.py [--n N] [--batch B] [--steps S]
+    torchrun --nproc-per-node 4 scripts/dist_minibatch.py [--vertices N] [--batch B] [--steps S]
 """
 import argparse
 import json
@@ -28,7 +28,7 @@ from paper_2212_05009_b200.runtime import DeviceRows  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=1 << 22)
+    ap.add_argument("--vertices", type=int, default=1 << 22)
     ap.add_argument("--batch", type=int, default=1 << 20)
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--shp-batches", type=int, default=4)
@@ -39,7 +39,7 @@ def main():
     torch.cuda.set_device(dev)
     dist.init_process_group(backend="gloo")
     t0 = time.perf_counter()
-    raw_p = synth.papers(args.seed, n=args.n)
+    raw_p = synth.papers(args.seed, n=args.vertices)
     n = raw_p.n_rows
     raw = gb.CsrMatrix(n, n, raw_p.row_offsets, raw_p.col_indices, raw_p.values)
     dims = synth.WORKLOADS["papers"][2]

@@ -44,7 +44,7 @@ def test_torchrun_minibatch_parity():
         pytest.skip("needs >= 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", "29913", str(ROOT / "scripts" / "dist_minibatch.py"),
-           "--n", "60000", "--batch", "20000", "--steps", "3", "--shp-batches", "2"]
+           "--vertices", "60000", "--batch", "20000", "--steps", "3", "--shp-batches", "2"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env={**os.environ, "OMP_NUM_THREADS": "1"})
     errs = [ln for ln in r.stderr.splitlines() if "Error" in ln and "elastic" not in ln]
     assert r.returncode == 0, r.stdout[-2000:] + "\n".join(errs[:20])
