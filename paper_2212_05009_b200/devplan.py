@@ -30,9 +30,9 @@ class _DevCsr:
     def __init__(self, a, dev):
         self.n = int(a.n_rows)
         self.rp_host = np.asarray(a.row_offsets, dtype=np.int64)
-        self.rp = torch.from_numpy(np.ascontiguousarray(self.rp_host)).to(dev)
-        self.ci = torch.from_numpy(np.ascontiguousarray(np.asarray(a.col_indices, dtype=np.int64))).to(dev)
-        self.val = torch.from_numpy(np.ascontiguousarray(np.asarray(a.values, dtype=np.float64))).to(dev)
+        self.rp = torch.from_numpy(np.array(self.rp_host)).to(dev)
+        self.ci = torch.from_numpy(np.array(a.col_indices, dtype=np.int64)).to(dev)
+        self.val = torch.from_numpy(np.array(a.values, dtype=np.float64)).to(dev)
 
 
 def _plan(dcsr: _DevCsr, owner: np.ndarray, p: int, dev):

@@ -65,6 +65,12 @@ class MessageRecord:
 
 @dataclass(frozen=True)
 class EpochMetrics:
+    """runtime.py:192-200.  Two extensions (defaults keep the reference's
+    constructor): `total_bytes`, the bytes the device actually moved, and
+    `reference_words`, the words the reference's schedule sends for the same
+    epoch — they differ from `total_words` only when reuse_fwd_aggregate drops
+    the layer-1 backward exchange (the log then lists the exchanges made)."""
+
     total_words: int
     max_words_per_proc: int
     avg_words_per_proc: float
@@ -72,6 +78,8 @@ class EpochMetrics:
     max_msgs_per_proc: int
     wallclock: float
     loss: float
+    total_bytes: int = 0
+    reference_words: int = 0
 
 
 @dataclass(frozen=True)
@@ -1015,14 +1023,21 @@ def _check_device(states) -> None:
         raise ValueError("in-process states must share one device; use distributed.py for one process per GPU")
 
 
-def _metrics_from_records(recs, p: int, wall: float, loss: float) -> EpochMetrics:
+def _metrics_from_records(recs, p: int, wall: float, loss: float, states=None) -> EpochMetrics:
     words = np.zeros(p, dtype=np.int64)
     msgs = np.zeros(p, dtype=np.int64)
+    nbytes = 0
     for r in recs:
         words[r.src] += r.words
         msgs[r.src] += 1
+        nbytes += int(getattr(r, "nbytes", 0))
+    ref = int(words.sum())
+    if states and states[0].skips_bwd_exchange(1):
+        st = states[0]  # the layer-1 backward exchange the reference also makes: rows × d_1 per plan pair
+        rows = sum(len(st.plan_bwd.send[m][q]) for m in range(p) for q in range(p) if m != q)
+        ref += rows * st.dims[1]
     return EpochMetrics(int(words.sum()), int(words.max()) if p else 0, float(words.sum() / p) if p else 0.0,
-                        int(msgs.sum()), int(msgs.max()) if p else 0, wall, loss)
+                        int(msgs.sum()), int(msgs.max()) if p else 0, wall, loss, nbytes, ref)
 
 
 def parallel_feedforward(states, net, scheduler: str = "round", epoch: int = 0):
@@ -1096,7 +1111,7 @@ def train_epochs(states, net, labels, epochs: int, mode=FullBatch(), scheduler: 
             lv = (losses.cpu().numpy() / n_lab).tolist()
             for e in range(epochs):
                 wall = evs[e].elapsed_time(evs[e + 1]) / 1e3
-                out.append(_metrics_from_records(_net_records(net, epoch=e), p, wall, lv[e]))
+                out.append(_metrics_from_records(_net_records(net, epoch=e), p, wall, lv[e], states))
             return out
         return _train_minibatch(states, net, labels, epochs, mode, dev)
 

@@ -303,3 +303,6 @@ def test_reuse_fwd_aggregate_against_oracle(directed, p):
     plan_b = states[0].plan_bwd
     bwd_rows = sum(len(plan_b.send[m][q]) for m in range(p) for q in range(p) if m != q)
     assert [m.total_words for m in metrics] == [w - bwd_rows * dims[1] for w in words]
+    # EpochMetrics also reports the reference's own word count for the same epoch
+    assert [m.reference_words for m in metrics] == list(words)
+    assert all(m.total_bytes > 0 for m in metrics) or p == 1
