@@ -155,6 +155,9 @@ int gcnb_dense_f32(const float* x, int32_t ldx, const int32_t* rows, int32_t n_r
  * everywhere, 2 = tcgen05 wherever the tile fits shared memory.  Both engines
  * meet the 1e-4 fp32 bar; they differ in the last bits. */
 int gcnb_set_dense_mode(int32_t mode);
+/* ΔW engine for contiguous row blocks: 1 (default) = Hᵀ in tensor memory
+ * (k_dw_tc2), 0 = both operands' hi/lo in shared memory (k_dw_tc); A/B knob */
+int gcnb_set_dw_mode(int32_t v2);
 /* *out = 1 when the tcgen05 engine serves act(X·W) for these widths. */
 int gcnb_dense_tc_applies(int32_t d_in, int32_t d_out, int32_t* out);
 /* H = relu(X·W) over rows 0..n_rows-1 (tcgen05 engine only) and its sign bits:

@@ -54,6 +54,7 @@ _SIGNATURES = {
         _c_int, [_vp, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _vp]),
     "gcnb_dense_f32": (_c_int, [_vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _vp]),
     "gcnb_set_dense_mode": (_c_int, [_c_int]),
+    "gcnb_set_dw_mode": (_c_int, [_c_int]),
     "gcnb_bwd_grid": (_c_int, [_c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_int)]),
     "gcnb_set_agg_shape": (_c_int, [_c_int, _c_int]),
     "gcnb_set_agg_gather": (_c_int, [_c_int]),
@@ -120,6 +121,8 @@ def load() -> ctypes.CDLL:
     _lib = lib
     if os.environ.get("GCNB_WATCHDOG_MS"):
         check(lib.gcnb_set_watchdog_ms(int(os.environ["GCNB_WATCHDOG_MS"])))
+    if os.environ.get("GCNB_DW_MODE"):
+        check(lib.gcnb_set_dw_mode(int(os.environ["GCNB_DW_MODE"])))
     if os.environ.get("GCNB_AGG_GATHER"):  # tuning knob (gcnb_set_agg_gather), e.g. for A/B bench runs
         check(lib.gcnb_set_agg_gather(int(os.environ["GCNB_AGG_GATHER"])))
     return lib

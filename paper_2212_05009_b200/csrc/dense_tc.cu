@@ -94,6 +94,7 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t base, int s, int rows) {
 
 namespace {
 int g_dense_mode = 0;  // 0 auto, 1 force SIMT, 2 force tensor core (where it applies)
+int g_dw_v2 = 1;       // 1: k_dw_tc2 (Hᵀ in TMEM) where it applies, 0: k_dw_tc (gcnb_set_dw_mode)
 }
 
 // Warp-specialised, transposed-orientation transform: the MMA computes
@@ -835,6 +836,239 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
   if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// k_dw_tc2: the same partials with Hᵀ (hi and lo) written to TENSOR memory as
+// the MMA A operand (tcgen05.mma with A from TMEM), contiguous row ranges by
+// TMA.  k_dw_tc keeps hi/lo of both operands in shared memory, so every tile
+// costs TMA writes + the converters' read/write + three MMAs' operand reads:
+// ~140 KB of shared-memory traffic per 32-row tile, which bounds it near 40 % of
+// HBM (ncu, products).  Here H arrives row-major (one TMA box per tile), the
+// converter thread of feature m reads its 32 values (conflict-free: a warp
+// reads one 128-byte row segment per step) and stores hi / lo to its own TMEM
+// lane; only A and lo(A) stay in shared memory.  Smaller stages (no lo(H), no
+// swizzle atoms for H) and no MMA reads of H: deeper pipeline, ~half the traffic.
+// TMEM columns: [0, 2·acc_cols) accumulators (double-buffered 256-row chunks,
+// drained into fp32 registers as in k_dw_tc), then 64 columns (hi | lo of the
+// 32-row K tile) per stage.
+//   warps 0-3  converter (Hᵀ → TMEM, lo(A) in place), then the epilogue
+//   warp 4     producer (one thread: TMA boxes for H and A)
+//   warp 5     TMEM owner; lane 0 issues the 3 × 4 MMAs of a tile
+constexpr int DW2_WARPS = 6;
+constexpr int DW2_THREADS = DW2_WARPS * 32;
+constexpr int DW2_MAX_STAGES = 6;
+
+namespace {
+struct Dw2Geom {
+  int na_a, hstride, h_bytes, a_bytes, st_bytes, stages, acc_cols;
+};
+
+__host__ __device__ inline Dw2Geom dw2_geom(int d_prev, int d_k) {
+  Dw2Geom g;
+  const int Np = (d_k + 15) & ~15;
+  g.na_a = (Np + 31) / 32;
+  g.hstride = (d_prev + 3) & ~3;
+  g.h_bytes = ((DW_T * g.hstride * 4 + 1023) / 1024) * 1024;  // A atoms stay 1024-byte aligned
+  g.a_bytes = g.na_a * DW_T * 128;
+  g.st_bytes = g.h_bytes + 2 * g.a_bytes;
+  g.acc_cols = Np <= 32 ? 32 : Np <= 64 ? 64 : Np <= 128 ? 128 : 256;
+  const int by_smem = (int)((size_t)(220 * 1024) / (size_t)g.st_bytes);
+  const int by_tmem = (512 - 2 * g.acc_cols) / 64;
+  int st = by_smem < by_tmem ? by_smem : by_tmem;
+  g.stages = st < DW2_MAX_STAGES ? st : DW2_MAX_STAGES;
+  return g;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(DW2_THREADS, 1)
+    k_dw_tc2(int d_prev, int d_k, int n_rows, float* __restrict__ partials, int n_slots,
+             const __grid_constant__ CUtensorMap tmh, const __grid_constant__ CUtensorMap tma_) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bars[3 * DW2_MAX_STAGES + 1];
+  __shared__ uint64_t accb[4];
+  __shared__ uint32_t tmem_base_slot;
+  const Dw2Geom g = dw2_geom(d_prev, d_k);
+  const int S = g.stages;
+  const int Np = (d_k + 15) & ~15;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = (n_rows + DW_T - 1) / DW_T;
+  const uint32_t acc_cols = g.acc_cols;
+  auto st_h = [&](int s) { return smem + s * g.st_bytes; };
+  auto st_a = [&](int s) { return smem + s * g.st_bytes + g.h_bytes; };
+  auto st_al = [&](int s) { return smem + s * g.st_bytes + g.h_bytes + g.a_bytes; };
+  auto bar = [&](int kind, int i) { return smem_u32(&bars[kind * DW2_MAX_STAGES + i]); };
+  const uint32_t b_done = smem_u32(&bars[3 * DW2_MAX_STAGES]);
+  if (smem_u32(smem) & 1023u) __trap();
+  // lo(A) pad columns (never loaded) must read as zero: clear once
+  for (int i = threadIdx.x; i < S * g.st_bytes / 16; i += DW2_THREADS)
+    reinterpret_cast<float4*>(smem)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(bar(0, i), 1);     // full: TMA
+      mbar_init(bar(1, i), 128);   // converted
+      mbar_init(bar(2, i), 1);     // empty: MMA commit
+    }
+    mbar_init(b_done, 1);
+    mbar_init(smem_u32(&accb[0]), 1);
+    mbar_init(smem_u32(&accb[1]), 1);
+    mbar_init(smem_u32(&accb[2]), 128);
+    mbar_init(smem_u32(&accb[3]), 128);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_async_smem();
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = tmem_base_slot;
+  auto a_col = [&](int s) { return tmem + 2 * acc_cols + (uint32_t)(64 * s); };
+
+  if (warp == 4) {
+    // ---------------- producer
+    if (lane == 0) {
+      const uint32_t tx = (uint32_t)(DW_T * g.hstride * 4 + g.a_bytes);
+      int t = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+        const int s = t % S;
+        if (t >= S) mbar_wait(bar(2, s), (uint32_t)(t / S - 1) & 1u);
+        mbar_expect_tx(bar(0, s), tx);
+        tma_load_2d(smem_u32(st_h(s)), &tmh, 0, tile * DW_T, bar(0, s));
+        for (int a = 0; a < g.na_a; ++a)
+          tma_load_2d(smem_u32(st_a(s)) + a * DW_T * 128, &tma_, 32 * a, tile * DW_T, bar(0, s));
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ---------------- MMA issuer: D[m][n] += Σ_k Hᵀ[m][k] · A[k][n]
+    if (lane == 0) {
+      const uint32_t idesc = idesc_tf32(128, Np) | (1u << 16);  // A from TMEM (K-major), B MN-major
+      const uint32_t kstep = 2 * 512;                            // 8 rows = two 4-row groups
+      int t = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+        const int s = t % S;
+        const int c = t / DW_CHUNK, buf = c & 1;
+        const bool first = t % DW_CHUNK == 0;
+        const bool last = t % DW_CHUNK == DW_CHUNK - 1 || tile + (int)gridDim.x >= n_tiles;
+        if (first && c >= 2) {
+          mbar_wait(smem_u32(&accb[2 + buf]), (uint32_t)(c / 2 - 1) & 1u);
+          tc_after_sync();
+        }
+        mbar_wait(bar(1, s), (uint32_t)(t / S) & 1u);
+        tc_after_sync();
+        const uint32_t acc = tmem + (uint32_t)buf * acc_cols;
+        const uint32_t ah = a_col(s), al = ah + 32;
+        const uint32_t ba = smem_u32(st_a(s)), bl = smem_u32(st_al(s));
+        for (int k = 0; k < DW_T / 8; ++k) {
+          const uint64_t dhi = desc_mn_sw32(ba + k * kstep);
+          mma_tf32_ts(acc, ah + 8 * k, dhi, idesc, (!first || k > 0) ? 1u : 0u);
+          mma_tf32_ts(acc, al + 8 * k, dhi, idesc, 1u);
+          mma_tf32_ts(acc, ah + 8 * k, desc_mn_sw32(bl + k * kstep), idesc, 1u);
+        }
+        mma_commit(bar(2, s));
+        if (last) mma_commit(smem_u32(&accb[buf]));
+      }
+      mma_commit(b_done);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- converter (warps 0-3: TMEM lanes 0-127 = features), then the epilogue
+    const int tid = threadIdx.x;
+    const int m = warp * 32 + lane;
+    const int ld_k = (d_k + 3) & ~3;
+    float* out = partials + (size_t)blockIdx.x * d_prev * ld_k + (size_t)m * ld_k;
+    float accr[DW_REG_COLS];
+#pragma unroll
+    for (int e = 0; e < DW_REG_COLS; ++e) accr[e] = 0.0f;
+    for (int c = DW_REG_COLS; c < ld_k; ++c)
+      if (m < d_prev) out[c] = 0.0f;
+    auto drain = [&](int c) {
+      const int buf = c & 1;
+      mbar_wait(smem_u32(&accb[buf]), (uint32_t)(c / 2) & 1u);
+      tc_after_sync();
+      const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)buf * acc_cols;
+#pragma unroll
+      for (int c0 = 0; c0 < 256; c0 += 8) {
+        if (c0 < Np) {
+          uint32_t v[8];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+              : "r"(base + (uint32_t)c0));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            if (c0 + e < DW_REG_COLS) accr[c0 + e] += __uint_as_float(v[e]);
+            else if (m < d_prev && c0 + e < ld_k) out[c0 + e] += __uint_as_float(v[e]);
+          }
+        }
+      }
+      tc_before_sync();
+      mbar_arrive(smem_u32(&accb[2 + buf]));
+    };
+    int t = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+      const int s = t % S;
+      mbar_wait(bar(0, s), (uint32_t)(t / S) & 1u);
+      // Hᵀ hi / lo of this K tile → TMEM lane m, columns [a_col(s), +32) / [+32, +64).
+      // (The MMAs of tile t - S, which read these columns, completed before the
+      // producer refilled stage s: its TMA waited on their commit.)
+      const float* hs = reinterpret_cast<const float*>(st_h(s));
+      const uint32_t ta = a_col(s) + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const float v = m < d_prev ? hs[(half * 16 + r) * g.hstride + m] : 0.0f;
+          hi[r] = __float_as_uint(v);
+          lo[r] = __float_as_uint(tf32_lo(v));
+        }
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+            ::"r"(ta + 16 * half), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]),
+            "r"(hi[6]), "r"(hi[7]), "r"(hi[8]), "r"(hi[9]), "r"(hi[10]), "r"(hi[11]), "r"(hi[12]), "r"(hi[13]),
+            "r"(hi[14]), "r"(hi[15])
+            : "memory");
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+            ::"r"(ta + 32 + 16 * half), "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]),
+            "r"(lo[6]), "r"(lo[7]), "r"(lo[8]), "r"(lo[9]), "r"(lo[10]), "r"(lo[11]), "r"(lo[12]), "r"(lo[13]),
+            "r"(lo[14]), "r"(lo[15])
+            : "memory");
+      }
+      lo_copy(st_al(s), st_a(s), g.a_bytes, tid);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      fence_async_smem();
+      tc_before_sync();
+      mbar_arrive(bar(1, s));
+      if ((t + 1) % DW_CHUNK == 0 && t + 1 >= 2 * DW_CHUNK) drain((t + 1) / DW_CHUNK - 2);
+    }
+    const int n_chunks = (t + DW_CHUNK - 1) / DW_CHUNK;
+    for (int c = std::max(0, t / DW_CHUNK - 1); c < n_chunks; ++c) drain(c);
+    if (n_tiles > (int)blockIdx.x) mbar_wait(b_done, 0);
+    tc_after_sync();
+    if (m < d_prev) {
+#pragma unroll
+      for (int e = 0; e < DW_REG_COLS; ++e)
+        if (e < ld_k) out[e] = accr[e];
+    }
+  }
+  {
+    const int ld_k = (d_k + 3) & ~3;
+    const size_t slot = (size_t)d_prev * ld_k;
+    for (int sl = blockIdx.x + gridDim.x; sl < n_slots; sl += gridDim.x)
+      for (size_t e = threadIdx.x; e < slot; e += DW2_THREADS) partials[sl * slot + e] = 0.0f;
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
 bool dw_tc_applies(int d_prev, int d_k) {
   if (g_dense_mode == 1) return false;
   return d_prev <= 128 && d_k <= 256 && dw_geom(d_k).stages >= 2;
@@ -853,6 +1087,19 @@ int launch_dw_tc(const float* h, int ldh, int d_prev, const float* a, int lda, i
   const bool tma = rows == nullptr && n_rows > 0 &&
                    tmap_2d(&tmh, h, d_prev, n_rows, ldh, 32, DW_T, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
                    tmap_2d(&tma_, a, d_k, n_rows, lda, 32, DW_T, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  const Dw2Geom g2 = dw2_geom(d_prev, d_k);
+  if (tma && g_dw_v2 && g2.stages >= 2) {
+    // Hᵀ in TMEM (k_dw_tc2): H as plain row-major boxes of the whole (padded) row
+    CUtensorMap tmh2;
+    std::memset(&tmh2, 0, sizeof(tmh2));
+    if (tmap_2d(&tmh2, h, d_prev, n_rows, ldh, g2.hstride, DW_T, CU_TENSOR_MAP_SWIZZLE_NONE)) {
+      const size_t smem2 = (size_t)g2.stages * g2.st_bytes;
+      cudaFuncSetAttribute(k_dw_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+      k_dw_tc2<<<grid, DW2_THREADS, smem2, st>>>(d_prev, d_k, n_rows, partials, n_slots, tmh2, tma_);
+      GCNB_AFTER_LAUNCH("bwd ΔW (tcgen05 3xTF32, Hᵀ in TMEM, TMA)");
+      return GCNB_OK;
+    }
+  }
   auto fn = tma ? k_dw_tc<true> : k_dw_tc<false>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fn<<<grid, DW_THREADS, smem, st>>>(h, ldh, d_prev, a, lda, d_k, rows, n_rows, partials, n_slots, tmh, tma_);
@@ -865,5 +1112,10 @@ int launch_dw_tc(const float* h, int ldh, int d_prev, const float* a, int lda, i
 extern "C" int gcnb_set_dense_mode(int32_t mode) {
   GCNB_REQUIRE(mode >= 0 && mode <= 2, "dense mode must be 0 (auto), 1 (SIMT) or 2 (tensor core)");
   gcnb::g_dense_mode = mode;
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_set_dw_mode(int32_t v2) {
+  gcnb::g_dw_v2 = v2 ? 1 : 0;
   return GCNB_OK;
 }
