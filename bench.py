@@ -262,7 +262,7 @@ def _oracle_one_epoch(o, ws, a, a_back, h0, ids, y, lr, threads):
     return [w - lr * dw for w, dw in zip(ws, dws)], loss, h[-1]
 
 
-REF_BUDGET_S = float(os.environ.get("GCNB_REF_BUDGET_S", "900"))
+REF_BUDGET_S = float(os.environ.get("GCNB_REF_BUDGET_S", "300"))
 SOAK_S = 1.5
 
 

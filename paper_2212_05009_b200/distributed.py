@@ -697,13 +697,16 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
     rng = np.random.default_rng([int(seed), 0x7B])
     n = raw.n_rows
     losses, walls, words = [], [], []
+    phases = {"draw": 0.0, "operator": 0.0, "setup": 0.0, "step": 0.0, "teardown": 0.0}
     ws = [np.asarray(w) for w in model.weights]
     for step in range(steps):
         torch.cuda.synchronize(device)
         dist.barrier()
         t0 = time.perf_counter()
         batch = np.sort(rng.choice(n, size=spec_batch, replace=False))
+        t1 = time.perf_counter()
         sub_hat = _batch_operator(raw, batch, device)
+        t2 = time.perf_counter()
         sub_labels = _local_labelset(labels, batch)
         if sub_labels is None:  # no labelled vertex: ΔW = 0, weights unchanged (runtime.py:620-625)
             losses.append(0.0)
@@ -713,9 +716,11 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
         m = GcnModel(tuple(model.dims), tuple(ws), model.activation, model.learning_rate)
         tr = DistributedTrainer(sub_hat, DeviceRows(features.feat, features.d, batch), np.asarray(owner)[batch], p, m,
                                 sub_labels, directed, device, timeout_ms=timeout_ms, overlap=False)
+        t3 = time.perf_counter()
         tr.enqueue_epoch(0)
         torch.cuda.synchronize(device)
         tr.check()
+        t4 = time.perf_counter()
         losses.append(float(tr.loss_total.item()) / len(sub_labels))
         ws = [np.asarray(w) for w in tr.st.weights]
         words.append(reference_words_per_epoch(tr.layout, tuple(model.dims)))
@@ -723,5 +728,11 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
         tr.close()        # unmap the peers' arenas ...
         dist.barrier()    # ... everywhere before any rank frees its own
         tr.arena.free()
-        walls.append(time.perf_counter() - t0)
+        t5 = time.perf_counter()
+        walls.append(t5 - t0)
+        if step > 0:  # the first step also pays one-time uploads
+            for k, v in (("draw", t1 - t0), ("operator", t2 - t1), ("setup", t3 - t2), ("step", t4 - t3),
+                         ("teardown", t5 - t4)):
+                phases[k] += v / max(steps - 1, 1)
+    train_minibatch.last_phases = {k: round(1e3 * v, 1) for k, v in phases.items()}
     return losses, walls, words, ws

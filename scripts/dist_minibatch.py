@@ -81,6 +81,7 @@ def main():
                "ms_per_step_median": round(1e3 * float(np.median(walls[1:] or walls)), 1),
                "ms_per_step_max_over_ranks_after_first": round(1e3 * float(mx[0]), 1),
                "words_per_step_all_ranks": int(tot[0].item() / args.steps), "losses": losses,
+               "rank0_phase_ms_per_step": getattr(distributed.train_minibatch, "last_phases", None),
                "parity_first_step": {"loss_gpu": losses[0], "loss_oracle": ref_loss,
                                      "loss_rel": abs(losses[0] - ref_loss) / abs(ref_loss)}}
         print(json.dumps(out), flush=True)
