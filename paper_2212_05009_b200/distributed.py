@@ -182,17 +182,31 @@ class _CAI:
 class Arena:
     """One cudaMalloc'd, IPC-exportable block carved into torch views."""
 
-    def __init__(self, offsets: dict, device):
+    def __init__(self, offsets: dict, device, capacity: int = 0):
         import torch
 
         self.off = offsets
         self.device = device
+        self.capacity = max(int(offsets["_total"]), int(capacity))
         ptr = ctypes.c_void_p()
         with torch.cuda.device(device):
-            _lib.call("gcnb_malloc", ctypes.byref(ptr), offsets["_total"])
+            _lib.call("gcnb_malloc", ctypes.byref(ptr), self.capacity)
             self.base = ptr.value
-            _lib.call("gcnb_memset_async", self.base, 0, offsets["_total"], None)
+            _lib.call("gcnb_memset_async", self.base, 0, self.capacity, None)
             torch.cuda.synchronize(device)
+
+    def reuse(self, offsets: dict) -> bool:
+        """Lay a new set of buffers over the same allocation (mini-batch steps):
+        zeroed again, same IPC handle, so peers keep their mappings."""
+        import torch
+
+        if offsets["_total"] > self.capacity:
+            return False
+        self.off = offsets
+        with torch.cuda.device(self.device):
+            _lib.call("gcnb_memset_async", self.base, 0, offsets["_total"], None)
+            torch.cuda.synchronize(self.device)
+        return True
 
     def tensor(self, name: str, shape, dtype):
         import torch
@@ -225,7 +239,8 @@ class DistributedTrainer:
     OVERLAP_MIN_BYTES = 4 << 20
 
     def __init__(self, a_hat, h0, owner, p: int, model, labels, directed: bool, device, timeout_ms: int = 20000,
-                 row_labels=None, overlap: bool | None = None, reuse_fwd_aggregate: bool = False):
+                 row_labels=None, overlap: bool | None = None, reuse_fwd_aggregate: bool = False,
+                 arena_cache: dict | None = None):
         """row_labels: optional per-vertex community labels for the locality
         layout of own rows (locality.py); None keeps ascending global ids.
         overlap: split each layer into interior rows (computed while the halo
@@ -260,7 +275,18 @@ class DistributedTrainer:
         n_own = len(layout.global_rows)
         self.off = arena_layout(n_own, layout.fwd.n_halo, layout.bwd.n_halo, dims, tf, p, n_pack)
         torch.cuda.set_device(device)
-        self.arena = Arena(self.off, device)
+        # arena_cache (mini-batch steps): keep one arena per rank, IPC-mapped by
+        # the peers once, and lay each step's buffers over it
+        self.arena_cache = arena_cache
+        if arena_cache is not None and arena_cache.get("arena") is not None and arena_cache["arena"].reuse(self.off):
+            self.arena = arena_cache["arena"]
+        else:
+            if arena_cache is not None and arena_cache.get("arena") is not None:
+                self._release_cached(arena_cache)
+            self.arena = Arena(self.off, device, capacity=int(self.off["_total"] * 1.5))
+            if arena_cache is not None:
+                arena_cache["arena"] = self.arena
+                arena_cache["peers"] = {}
         from .runtime import DeviceRows
 
         rows_h0 = (h0.take(layout.global_rows if h0.ids is None else h0.ids[layout.global_rows])
@@ -288,13 +314,21 @@ class DistributedTrainer:
         infos = [None] * p
         dist.all_gather_object(infos, info)
         self.peer_base = {}
+        mapped = arena_cache.setdefault("peers", {}) if arena_cache is not None else None
         for r, inf in enumerate(infos):
             if r == self.rank:
                 self.peer_base[r] = a.base
                 continue
+            if mapped is not None and r in mapped and mapped[r][0] == inf["handle"]:
+                self.peer_base[r] = mapped[r][1]  # the peer kept its arena: mapping still valid
+                continue
+            if mapped is not None and r in mapped:
+                _lib.call("gcnb_ipc_close_handle", mapped.pop(r)[1])
             ptr = ctypes.c_void_p()
             _lib.call("gcnb_ipc_open_handle", inf["handle"], ctypes.byref(ptr))
             self.peer_base[r] = ptr.value
+            if mapped is not None:
+                mapped[r] = (inf["handle"], ptr.value)
         self.infos = infos
         self.fwd_bases = [None] + [{r: (self.peer_base[r] + infos[r]["off"][f"xext{k}"], infos[r]["n_own"])
                                     for r in range(p)} for k in range(1, L + 1)]
@@ -444,7 +478,18 @@ class DistributedTrainer:
             raise _lib.CommError(f"rank {self.rank}: a halo/allreduce doorbell timed out "
                                  f"(after {self.timeout_ms} ms)")
 
+    @staticmethod
+    def _release_cached(cache: dict) -> None:
+        for _, ptr in cache.get("peers", {}).values():
+            _lib.call("gcnb_ipc_close_handle", ptr)
+        cache["peers"] = {}
+        cache["arena"].free()
+        cache["arena"] = None
+
     def close(self) -> None:
+        if self.arena_cache is not None:  # mappings and arena live on in the cache
+            self.peer_base = {}
+            return
         for r, base in self.peer_base.items():
             if r != self.rank:
                 _lib.call("gcnb_ipc_close_handle", base)
@@ -699,6 +744,7 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
     losses, walls, words = [], [], []
     phases = {"draw": 0.0, "operator": 0.0, "setup": 0.0, "step": 0.0, "teardown": 0.0}
     ws = [np.asarray(w) for w in model.weights]
+    cache: dict = {}
     for step in range(steps):
         torch.cuda.synchronize(device)
         dist.barrier()
@@ -715,7 +761,7 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
             continue
         m = GcnModel(tuple(model.dims), tuple(ws), model.activation, model.learning_rate)
         tr = DistributedTrainer(sub_hat, DeviceRows(features.feat, features.d, batch), np.asarray(owner)[batch], p, m,
-                                sub_labels, directed, device, timeout_ms=timeout_ms, overlap=False)
+                                sub_labels, directed, device, timeout_ms=timeout_ms, overlap=False, arena_cache=cache)
         t3 = time.perf_counter()
         tr.enqueue_epoch(0)
         torch.cuda.synchronize(device)
@@ -724,15 +770,16 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
         losses.append(float(tr.loss_total.item()) / len(sub_labels))
         ws = [np.asarray(w) for w in tr.st.weights]
         words.append(reference_words_per_epoch(tr.layout, tuple(model.dims)))
-        dist.barrier()
-        tr.close()        # unmap the peers' arenas ...
-        dist.barrier()    # ... everywhere before any rank frees its own
-        tr.arena.free()
+        dist.barrier()    # every rank is done with this step's buffers before any re-lays its arena
+        tr.close()
         t5 = time.perf_counter()
         walls.append(t5 - t0)
         if step > 0:  # the first step also pays one-time uploads
             for k, v in (("draw", t1 - t0), ("operator", t2 - t1), ("setup", t3 - t2), ("step", t4 - t3),
                          ("teardown", t5 - t4)):
                 phases[k] += v / max(steps - 1, 1)
+    dist.barrier()
+    if cache.get("arena") is not None:
+        DistributedTrainer._release_cached(cache)
     train_minibatch.last_phases = {k: round(1e3 * v, 1) for k, v in phases.items()}
     return losses, walls, words, ws
