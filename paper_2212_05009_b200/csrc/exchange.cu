@@ -47,28 +47,13 @@ __global__ void __launch_bounds__(NT) k_pack(const float4* __restrict__ X4, int 
                                              int signal) {
   const int total = a.seg_ptr[a.n_seg];
   const long long work = (long long)total * c4;
-  const long long stride = (long long)gridDim.x * NT;
-  // four independent gathers in flight per thread before their (remote) stores
-  for (long long t0 = blockIdx.x * (long long)NT + threadIdx.x; t0 < work; t0 += 4 * stride) {
-    float4 v[4];
-    int seg[4], row[4], chn[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const long long t = t0 + u * stride;
-      seg[u] = -1;
-      if (t < work) {
-        const int e = (int)(t / c4);
-        chn[u] = (int)(t - (long long)e * c4);
-        int sg = 0;
-        while (e >= a.seg_ptr[sg + 1]) ++sg;
-        seg[u] = sg;
-        row[u] = e - a.seg_ptr[sg];
-        v[u] = __ldg(X4 + (size_t)__ldg(idx + e) * ldx4 + chn[u]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (seg[u] >= 0) reinterpret_cast<float4*>(a.dst[seg[u]])[(size_t)row[u] * ldd4 + chn[u]] = v[u];
+  for (long long t = blockIdx.x * (long long)NT + threadIdx.x; t < work; t += (long long)gridDim.x * NT) {
+    const int e = (int)(t / c4);
+    const int ch = (int)(t - (long long)e * c4);
+    int s = 0;
+    while (e >= a.seg_ptr[s + 1]) ++s;
+    const float4 v = __ldg(X4 + (size_t)__ldg(idx + e) * ldx4 + ch);
+    reinterpret_cast<float4*>(a.dst[s])[(size_t)(e - a.seg_ptr[s]) * ldd4 + ch] = v;
   }
   if (!signal) return;
   // The block's (possibly remote) stores happen-before thread 0's system-scope
@@ -402,10 +387,9 @@ extern "C" int gcnb_pack_rows_f32(const float* x, int32_t ldx, int32_t d, const 
   GCNB_REQUIRE(total == 0 || (idx && aligned16(x)), "pack: index list and 16-byte aligned source required");
   const int c4 = round4(d) / 4;
   const long long work = (long long)total * c4;
-  // ~16 chunks per thread (4 rounds of 4 gathers in flight): fewer blocks → fewer
-  // system fences and last-block arrivals, the latency floor of small exchanges
-  // (up to 16·NT chunks a single block: one fence, no election)
-  const int grid = (int)std::max<long long>(1, std::min<long long>((work + 16 * NT - 1) / (16 * NT), num_sms()));
+  // a few rows per thread: fewer blocks → fewer fences and counter arrivals
+  // (up to 4·NT chunks a single block: one fence, no last-block election)
+  const int grid = (int)std::max<long long>(1, std::min<long long>((work + 4 * NT - 1) / (4 * NT), num_sms() * 2));
   k_pack<<<grid, NT, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4*>(x), ldx / 4, c4, idx, a, ld_dst / 4,
                                                 counter, signal);
   GCNB_AFTER_LAUNCH("pack rows");

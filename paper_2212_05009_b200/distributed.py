@@ -760,8 +760,23 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
             words.append(0)
             continue
         m = GcnModel(tuple(model.dims), tuple(ws), model.activation, model.learning_rate)
+        prof = None
+        if os.environ.get("GCNB_PROFILE_SETUP") and step == 1 and dist.get_rank() == 0:
+            import cProfile
+
+            prof = cProfile.Profile()
+            prof.enable()
         tr = DistributedTrainer(sub_hat, DeviceRows(features.feat, features.d, batch), np.asarray(owner)[batch], p, m,
                                 sub_labels, directed, device, timeout_ms=timeout_ms, overlap=False, arena_cache=cache)
+        if prof is not None:
+            import io
+            import pstats
+            import sys
+
+            prof.disable()
+            buf = io.StringIO()
+            pstats.Stats(prof, stream=buf).sort_stats("cumulative").print_stats(30)
+            print(buf.getvalue(), file=sys.stderr, flush=True)
         t3 = time.perf_counter()
         tr.enqueue_epoch(0)
         torch.cuda.synchronize(device)
