@@ -81,3 +81,54 @@ def test_reference_suite_against_device_path(results):
                 continue  # fp32 rounding (or bit-exact equality with the fp64 oracle)
         bad.append((r["nodeid"], r["longrepr"][-600:]))
     assert not bad, bad
+
+
+def test_reference_cli_runs_on_the_device_path(tmp_path):
+    """gcnpart's own experiment driver (cli.run_experiment, cli.py:208-318)
+    with compat.install(): the same report as the unmodified reference — plan,
+    cuts, every epoch's words and messages identical, losses within 1e-4 —
+    for RP and HP partitions of a 400-vertex graph at p = 4."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import importlib
+
+    for root in (REF, Path("/root/reference/pkg/src")):
+        if (root / "gcnpart").exists():
+            sys.path.insert(0, str(root))
+            break
+    else:
+        pytest.skip("gcnpart is not installed under baseline/_ref")
+    gcnpart = importlib.import_module("gcnpart")
+    cli = importlib.import_module("gcnpart.cli")
+    from paper_2212_05009_b200 import compat
+
+    import numpy as np
+
+    rng = np.random.default_rng(5)
+    n = 400
+    edges = set()
+    while len(edges) < 1600:
+        u, v = (int(x) for x in rng.integers(0, n, 2))
+        if u != v:
+            edges.add((min(u, v), max(u, v)))
+    g = tmp_path / "g.txt"
+    g.write_text("\n".join(f"{u} {v}" for u, v in sorted(edges)) + "\n")
+    docs = {}
+    for side in ("reference", "device"):
+        if side == "device":
+            compat.install(gcnpart)
+        try:
+            cfg = cli.ExperimentConfig(graph=str(g), p=4, partitioners=("rp", "hp"), epochs=3, dims=(8, 8, 4),
+                                       out=str(tmp_path / side), seed=0)
+            docs[side] = cli.run_experiment(cfg)
+        finally:
+            if side == "device":
+                compat.uninstall(gcnpart)
+    for ref, dev in zip(docs["reference"]["runs"], docs["device"]["runs"]):
+        assert ref["partitioner"] == dev["partitioner"]
+        assert ref["plan"] == dev["plan"] and ref["cuts"] == dev["cuts"] and ref["partition"] == dev["partition"]
+        for er, ed in zip(ref["epochs"], dev["epochs"]):
+            for k in ("total_words", "max_words_per_proc", "avg_words_per_proc", "total_msgs", "max_msgs_per_proc"):
+                assert er[k] == ed[k], (k, er[k], ed[k])
+            assert abs(er["loss"] - ed["loss"]) <= 1e-4 * abs(er["loss"])
