@@ -249,6 +249,50 @@ int gcnb_loss_grad_pack_f32(const float* h, int32_t ldh, int32_t n_rows, int32_t
                             double* loss_sum, const int32_t* map_ptr, const int32_t* map, float* const* dst,
                             uint64_t* const* flags, int32_t n_seg, int32_t ldd, int32_t* counter, void* stream);
 
+/* A halo pack fused into the epilogue of the kernel that produces the rows
+ * (runtime.py:289-294 / 336-341 + SimNetwork.send, without the separate
+ * gcnb_pack_rows_f32 launch and its re-read of the rows): own row r, as the
+ * kernel stores it, is also stored into every receiver slot
+ * map[map_ptr[r] .. map_ptr[r+1]) names ({segment, position} int pairs; slot =
+ * dst[segment] + position*ldd floats, a peer-mapped NVLink address), and after
+ * all of the launch's stores are visible system-wide the last block
+ * increments *flags[s] for every segment, as gcnb_pack_rows_f32 does.
+ * map_ptr (n_rows+1) and map live on the device; dst and flags are host arrays
+ * of n_seg device pointers (flags may be NULL); counter is a zero-initialised
+ * device int that no concurrently running kernel shares.  pack == NULL or
+ * n_seg == 0: plain kernel. */
+typedef struct gcnb_halo_pack {
+  const int32_t* map_ptr;
+  const int32_t* map;
+  float* const* dst;
+  uint64_t* const* flags;
+  int32_t n_seg;
+  int32_t ldd;
+  int32_t* counter;
+} gcnb_halo_pack;
+
+/* gcnb_dense_f32 over own rows 0..n_rows-1 (bits != NULL: gcnb_dense_bits_f32)
+ * with the produced rows packed into the receivers' halos: the transform of a
+ * transform-first layer (T^k = H^{k-1}·W^k, runtime.py:297-306 reordered) or the
+ * dense half of a split forward layer (H^k = act(Y·W^k)). */
+int gcnb_dense_pack_f32(const float* x, int32_t ldx, int32_t n_rows, int32_t d_in, const float* w, int32_t d_out,
+                        float* y, int32_t ldy, int32_t act, uint32_t* bits, int32_t ld_bits,
+                        const gcnb_halo_pack* pack, void* stream);
+/* gcnb_fwd_layer_f32 (w != NULL) over own rows 0..n_rows-1 with H packed. */
+int gcnb_fwd_layer_pack_f32(const int32_t* row_ptr, const int32_t* col, const float* val, int32_t n_rows,
+                            const float* x, int32_t ldx, int32_t d_in, const float* w, int32_t d_out, float* h,
+                            int32_t ldh, int32_t act, const gcnb_halo_pack* pack, void* stream);
+/* gcnb_bwd_layer_f32 over own rows 0..n_rows-1 with G_prev packed (g_prev != NULL). */
+int gcnb_bwd_layer_pack_f32(const int32_t* row_ptr, const int32_t* col, const float* val, int32_t n_rows,
+                            const float* g, int32_t ldg, int32_t d_k, const float* h_prev, int32_t ldhp,
+                            int32_t d_prev, const float* w, float* g_prev, int32_t ldgp, int32_t act,
+                            float* dw_partials, float* workspace, const gcnb_halo_pack* pack, void* stream);
+/* gcnb_bwd_epilogue_f32 over own rows 0..n_rows-1 with G_prev packed. */
+int gcnb_bwd_epilogue_pack_f32(const float* agg, int32_t ldagg, int32_t d_k, const float* h_prev, int32_t ldhp,
+                               int32_t d_prev, const float* w, float* g_prev, int32_t ldgp, int32_t act,
+                               const uint32_t* hbits, int32_t ld_hbits, int32_t n_rows, float* dw_partials,
+                               const gcnb_halo_pack* pack, void* stream);
+
 /* allreduce_sum (runtime.py:147-157): out = bufs[0] + bufs[1] + ... in
  * ascending rank order (bit-identical on every rank).  bufs is a host array of
  * p device pointers (local or peer-mapped). */

@@ -76,6 +76,14 @@ _SIGNATURES = {
     "gcnb_loss_grad_pack_f32": (
         _c_int, [_vp, _c_int, _c_int, _c_int, _vp, _f64, _vp, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _c_int,
                  _c_int, _vp, _vp]),
+    "gcnb_dense_pack_f32": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int,
+                                     _vp, _vp]),
+    "gcnb_fwd_layer_pack_f32": (_c_int, [_vp, _vp, _vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp, _c_int,
+                                         _c_int, _vp, _vp]),
+    "gcnb_bwd_layer_pack_f32": (_c_int, [_vp, _vp, _vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _vp,
+                                         _c_int, _c_int, _vp, _vp, _vp, _vp]),
+    "gcnb_bwd_epilogue_pack_f32": (_c_int, [_vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp,
+                                            _c_int, _c_int, _vp, _vp, _vp]),
     "gcnb_sum_buffers_f32": (_c_int, [_vp, _c_int, _c_i64, _vp, _vp]),
     "gcnb_sum_buffers_f64": (_c_int, [_vp, _c_int, _c_i64, _vp, _vp]),
     "gcnb_sgd_f32": (_c_int, [_vp, _vp, _c_i64, _f32, _vp]),
@@ -155,6 +163,23 @@ def ptr_array(ptrs) -> ctypes.Array:
     for i, p in enumerate(ptrs):
         arr[i] = p
     return arr
+
+
+class HaloPack(ctypes.Structure):
+    """gcnb_halo_pack (include/gcnb.h): a halo pack fused into a producer's epilogue."""
+
+    _fields_ = [("map_ptr", ctypes.c_void_p), ("map", ctypes.c_void_p), ("dst", ctypes.c_void_p),
+                ("flags", ctypes.c_void_p), ("n_seg", ctypes.c_int32), ("ldd", ctypes.c_int32),
+                ("counter", ctypes.c_void_p)]
+
+
+def halo_pack(map_ptr: int, map_: int, dsts, flags, ldd: int, counter: int):
+    """A HaloPack (by reference) plus the host arrays it points at (keep both alive for the call)."""
+    d = ptr_array(dsts)
+    f = ptr_array(flags) if flags is not None else None
+    hp = HaloPack(map_ptr, map_, ctypes.cast(d, ctypes.c_void_p),
+                  ctypes.cast(f, ctypes.c_void_p) if f is not None else None, len(dsts), ldd, counter)
+    return ctypes.byref(hp), (hp, d, f)
 
 
 def int_array(vals) -> ctypes.Array:

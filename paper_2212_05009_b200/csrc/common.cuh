@@ -12,6 +12,8 @@
 
 namespace gcnb {
 
+struct EpiPack;  // epipack.cuh
+
 constexpr int NT = 256;          // threads per block for the row kernels
 constexpr int WARPS = NT / 32;
 constexpr int RPT_MAX = 8;       // output rows per thread in the tile GEMMs
@@ -34,7 +36,7 @@ int launch_agg_far(const int32_t* row_ptr, const int32_t* nnear, const void* ent
 // dense.cu: register-blocked SIMT transform for the wide dense layers
 bool dense_blocked_applies(int d_in, int d_out);
 int launch_dense_blocked(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
-                         float* y, int ldy, int act, cudaStream_t st);
+                         float* y, int ldy, int act, cudaStream_t st, const EpiPack* pk = nullptr);
 // dense_tc.cu: tcgen05 3xTF32 transform for the wide dense layers
 bool dense_tc_applies(int d_in, int d_out);
 // w_nk != nullptr: B = w_nk stored N×K (row stride ld_wnk) instead of w (K×N);
@@ -45,7 +47,7 @@ bool dense_tc_applies(int d_in, int d_out);
 int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
                     float* y, int ldy, int act, cudaStream_t st, const float* w_nk = nullptr, int ld_wnk = 0,
                     const float* hmask = nullptr, int ldhm = 0, const uint32_t* hbits = nullptr, int ld_hbits = 0,
-                    uint32_t* bits_out = nullptr, int ld_bits_out = 0);
+                    uint32_t* bits_out = nullptr, int ld_bits_out = 0, const EpiPack* pk = nullptr);
 bool dw_tc_applies(int d_prev, int d_k);
 int dw_tc_grid(int n_rows);
 int launch_dw_tc(const float* h, int ldh, int d_prev, const float* a, int lda, int d_k, const int* rows, int n_rows,

@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "epipack.cuh"
 
 namespace gcnb {
 
@@ -19,7 +20,7 @@ constexpr int DT_M = 8, DT_N = 8, DT_BK = 16;
 
 __global__ void __launch_bounds__(NT) k_dense(const float4* __restrict__ X4, int ldx4, const int* __restrict__ rows,
                                               int n_rows, int K, const float4* __restrict__ W4, int ldN, int N,
-                                              float* __restrict__ Y, int ldy, int act) {
+                                              float* __restrict__ Y, int ldy, int act, const EpiPack pk) {
   extern __shared__ __align__(16) float sm[];
   const int K4 = (K + 3) & ~3;
   float* Ws = sm;                                  // K4 × ldN (rows >= K zero)
@@ -92,6 +93,11 @@ __global__ void __launch_bounds__(NT) k_dense(const float4* __restrict__ X4, int
       }
     }
   }
+  if (pk.map_ptr) {
+    __syncthreads();
+    epi_forward(pk, Y, ldy, rows, n_rows, BM, ldN / 4);
+    epi_signal(pk);
+  }
 }
 
 // Used by gcnb_dense_f32 when the blocked kernel applies (returns false otherwise).
@@ -101,7 +107,7 @@ bool dense_blocked_applies(int d_in, int d_out) {
 }
 
 int launch_dense_blocked(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
-                         float* y, int ldy, int act, cudaStream_t st) {
+                         float* y, int ldy, int act, cudaStream_t st, const EpiPack* pk) {
   const int ldN = round4(d_out), K4 = round4(d_in);
   const int CG = (ldN + DT_N - 1) / DT_N;
   const int RG = NT / CG;
@@ -117,7 +123,8 @@ int launch_dense_blocked(const float* x, int ldx, const int* rows, int n_rows, i
   const int tiles = (n_rows + BM - 1) / BM;
   const int grid = std::max(1, std::min(tiles, per_sm * num_sms()));
   k_dense<<<grid, NT, smem, st>>>(reinterpret_cast<const float4*>(x), ldx / 4, rows, n_rows, d_in,
-                                  reinterpret_cast<const float4*>(w), ldN, d_out, y, ldy, act);
+                                  reinterpret_cast<const float4*>(w), ldN, d_out, y, ldy, act,
+                                  pk ? *pk : EpiPack{});
   GCNB_AFTER_LAUNCH("dense (blocked)");
   return GCNB_OK;
 }

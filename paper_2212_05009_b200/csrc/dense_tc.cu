@@ -21,6 +21,7 @@
 #include <cstdio>
 
 #include "common.cuh"
+#include "epipack.cuh"
 #include "sync.cuh"
 
 namespace gcnb {
@@ -175,7 +176,8 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
     k_dense_tc(const float* __restrict__ X, int ldx, const int* __restrict__ rows, int n_rows, int K,
                const float* __restrict__ W, int ldw, int w_nk, int M, int NT_, int S, float* __restrict__ Y,
                int ldy, const float* __restrict__ Hm, int ldhm, uint32_t* __restrict__ bits_out, int ld_bits,
-               const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmm) {
+               const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmm,
+               const EpiPack pk) {
   constexpr bool MASKED = MK != 0;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[4 * DT_MAX_STAGES + 4];
@@ -429,6 +431,8 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
+  epi_forward(pk, Y, ldy, rows, n_rows, NT_, mpad / 4);
+  epi_signal(pk);
   if (warp == 15) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
@@ -510,7 +514,9 @@ bool tmap_2d(CUtensorMap* m, const float* base, int cols, int n_rows, int ld, in
 
 int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_in, const float* w, int d_out,
                     float* y, int ldy, int act, cudaStream_t st, const float* w_nk, int ld_wnk, const float* hmask,
-                    int ldhm, const uint32_t* hbits, int ld_hbits, uint32_t* bits_out, int ld_bits_out) {
+                    int ldhm, const uint32_t* hbits, int ld_hbits, uint32_t* bits_out, int ld_bits_out,
+                    const EpiPack* pk) {
+  GCNB_REQUIRE(!pk || !pk->map_ptr || rows == nullptr, "dense (tcgen05): a fused halo pack needs rows 0..n-1");
   const int mk = hbits ? 2 : hmask ? 1 : 0;
   const int mpad = (d_out + 3) & ~3;
   const int mask_row = mk == 2 ? ld_hbits : mk == 1 ? mpad : 0;
@@ -535,7 +541,7 @@ int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_
   GCNB_REQUIRE(nt > 0, "dense (tcgen05): widths %d -> %d not supported", d_in, d_out);
   const bool relu = act == GCNB_ACT_RELU;
   using Fn = void (*)(const float*, int, const int*, int, int, const float*, int, int, int, int, int, float*, int,
-                      const float*, int, uint32_t*, int, const CUtensorMap, const CUtensorMap);
+                      const float*, int, uint32_t*, int, const CUtensorMap, const CUtensorMap, const EpiPack);
 #define GCNB_DT_PICK(T)                                                                              \
   (mk == 2 ? (relu ? k_dense_tc<true, 2, T> : k_dense_tc<false, 2, T>)                               \
            : mk == 1 ? (relu ? k_dense_tc<true, 1, T> : k_dense_tc<false, 1, T>)                     \
@@ -547,7 +553,7 @@ int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_
   const int grid = std::max(1, std::min(tiles, num_sms()));
   fn<<<grid, DT_THREADS, smem, st>>>(x, ldx, rows, n_rows, d_in, w_nk ? w_nk : w, w_nk ? ld_wnk : round4(d_out),
                                      w_nk ? 1 : 0, d_out, nt, stages, y, ldy, mptr, mld, bits_out, ld_bits_out, tmx,
-                                     tmm);
+                                     tmm, pk ? *pk : EpiPack{});
   GCNB_AFTER_LAUNCH(tma ? "dense (tcgen05 3xTF32, TMA)" : "dense (tcgen05 3xTF32)");
   return GCNB_OK;
 }

@@ -16,6 +16,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "epipack.cuh"
 
 namespace gcnb {
 
@@ -25,10 +26,6 @@ struct PackArgs {
   int seg_ptr[GCNB_MAX_PEERS + 1];
   int n_seg;
 };
-
-__device__ __forceinline__ void red_release_sys_add(unsigned long long* p, unsigned long long v) {
-  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
@@ -102,50 +99,6 @@ __global__ void k_wait(const unsigned long long* flags, WaitArgs a, unsigned lon
       return;
     }
     __nanosleep(64);
-  }
-}
-
-// Halo pack fused into a producing kernel's epilogue (north_star subsystem 2):
-// row r of the output, as it is stored, is also stored into every receiver's
-// halo slot that the plan assigns to it (map[map_ptr[r] .. map_ptr[r+1]) =
-// {segment, position}; segment s is receiver s's halo block for this rank, a
-// peer-mapped NVLink address), and once every block's stores are visible the
-// last block rings the receivers' doorbells — the k_pack protocol without the
-// separate launch and without re-reading the rows.
-struct EpiPack {
-  float4* dst[GCNB_MAX_PEERS];
-  unsigned long long* flag[GCNB_MAX_PEERS];
-  const int* map_ptr;
-  const int2* map;
-  int* counter;
-  int n_seg;
-  int ldd4;
-};
-
-__device__ __forceinline__ void epi_store(const EpiPack& pk, int row, int ch, float4 v) {
-  if (!pk.map_ptr) return;
-  const int e1 = __ldg(pk.map_ptr + row + 1);
-  for (int e = __ldg(pk.map_ptr + row); e < e1; ++e) {
-    const int2 m = __ldg(pk.map + e);
-    pk.dst[m.x][(size_t)m.y * pk.ldd4 + ch] = v;
-  }
-}
-
-// All threads of the block call this at the end of the kernel.
-__device__ __forceinline__ void epi_signal(const EpiPack& pk) {
-  if (!pk.map_ptr) return;
-  __syncthreads();
-  __shared__ int last;
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    last = (atomicAdd(pk.counter, 1) == (int)gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence_system();
-    *pk.counter = 0;
-    for (int s = 0; s < pk.n_seg; ++s)
-      if (pk.flag[s]) red_release_sys_add(pk.flag[s], 1ull);
   }
 }
 
@@ -431,27 +384,35 @@ extern "C" int gcnb_loss_grad_f32(const float* h, int32_t ldh, int32_t n_rows, i
                    pk);
 }
 
+namespace gcnb {
+int make_epipack(EpiPack* pk, const int32_t* map_ptr, const int32_t* map, float* const* dst, uint64_t* const* flags,
+                 int32_t n_seg, int32_t ldd, int32_t* counter) {
+  *pk = EpiPack{};
+  GCNB_REQUIRE(n_seg >= 0 && n_seg <= GCNB_MAX_PEERS, "pack: n_seg=%d out of range", n_seg);
+  if (n_seg == 0) return GCNB_OK;
+  GCNB_REQUIRE(map_ptr && map && dst && counter && ldd % 4 == 0, "pack: null or inconsistent pack arguments");
+  pk->map_ptr = map_ptr;
+  pk->map = reinterpret_cast<const int2*>(map);
+  pk->counter = counter;
+  pk->n_seg = n_seg;
+  pk->ldd4 = ldd / 4;
+  for (int s = 0; s < n_seg; ++s) {
+    GCNB_REQUIRE(dst[s] && aligned16(dst[s]), "pack: destination %d invalid", s);
+    pk->dst[s] = reinterpret_cast<float4*>(dst[s]);
+    pk->flag[s] = reinterpret_cast<unsigned long long*>(flags ? flags[s] : nullptr);
+  }
+  return GCNB_OK;
+}
+}  // namespace gcnb
+
 extern "C" int gcnb_loss_grad_pack_f32(const float* h, int32_t ldh, int32_t n_rows, int32_t d, const int32_t* label,
                                        double inv_n_labeled, float* g, int32_t ldg, int32_t act, double* scratch,
                                        double* loss_sum, const int32_t* map_ptr, const int32_t* map,
                                        float* const* dst, uint64_t* const* flags, int32_t n_seg, int32_t ldd,
                                        int32_t* counter, void* stream) {
-  GCNB_REQUIRE(n_seg >= 0 && n_seg <= GCNB_MAX_PEERS, "loss pack: n_seg=%d out of range", n_seg);
-  GCNB_REQUIRE(n_seg == 0 || (map_ptr && map && dst && flags && counter && ldd % 4 == 0 && ldd >= ldg),
-               "loss pack: null or inconsistent pack arguments");
-  EpiPack pk{};
-  if (n_seg > 0) {
-    pk.map_ptr = map_ptr;
-    pk.map = reinterpret_cast<const int2*>(map);
-    pk.counter = counter;
-    pk.n_seg = n_seg;
-    pk.ldd4 = ldd / 4;
-    for (int s = 0; s < n_seg; ++s) {
-      GCNB_REQUIRE(dst[s] && aligned16(dst[s]), "loss pack: destination %d invalid", s);
-      pk.dst[s] = reinterpret_cast<float4*>(dst[s]);
-      pk.flag[s] = reinterpret_cast<unsigned long long*>(flags ? flags[s] : nullptr);
-    }
-  }
+  GCNB_REQUIRE(n_seg == 0 || ldd >= ldg, "loss pack: destination stride below the row stride");
+  EpiPack pk;
+  if (int rc = make_epipack(&pk, map_ptr, map, dst, flags, n_seg, ldd, counter)) return rc;
   return loss_grad(h, ldh, n_rows, d, label, inv_n_labeled, g, ldg, act, scratch, loss_sum, (cudaStream_t)stream,
                    pk);
 }

@@ -19,6 +19,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "epipack.cuh"
 
 namespace gcnb {
 
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(NT) k_fwd_gemm(const int* __restrict__ rp, con
                                                  const float* __restrict__ val, const int* __restrict__ rows,
                                                  int n_rows, const float* __restrict__ X, int ldx, int d_in,
                                                  const float* __restrict__ W, int d_out, float* __restrict__ H,
-                                                 int ldh, int act, int T) {
+                                                 int ldh, int act, int T, const EpiPack pk) {
   extern __shared__ __align__(16) float smem[];
   const int ld_in = (d_in + 3) & ~3;
   const int ld_out = (d_out + 3) & ~3;
@@ -434,6 +435,8 @@ __global__ void __launch_bounds__(NT) k_fwd_gemm(const int* __restrict__ rp, con
     }
     __syncthreads();
   }
+  epi_forward(pk, H, ldh, rows, n_rows, T, (W ? ld_out : ld_in) / 4);
+  epi_signal(pk);
 }
 
 // ---------------------------------------------------------------------------
@@ -445,7 +448,7 @@ __global__ void __launch_bounds__(NT) k_bwd(const int* __restrict__ rp, const in
                                             int n_rows, const float* __restrict__ G, int ldg, int d_k,
                                             const float* __restrict__ Hp, int ldhp, int d_prev,
                                             const float* __restrict__ W, float* __restrict__ Gp, int ldgp,
-                                            int act, float* __restrict__ partials, int T) {
+                                            int act, float* __restrict__ partials, int T, const EpiPack pk) {
   extern __shared__ __align__(16) float smem[];
   const int ld_k = (d_k + 3) & ~3;
   const int ld_p = (d_prev + 3) & ~3;
@@ -527,6 +530,10 @@ __global__ void __launch_bounds__(NT) k_bwd(const int* __restrict__ rp, const in
       }
     }
     __syncthreads();
+  }
+  if (GP) {
+    epi_forward(pk, Gp, ldgp, rows, n_rows, T, c4p);
+    epi_signal(pk);
   }
   float* part = partials + (size_t)blockIdx.x * d_prev * ld_k;
   if (RS > 1) {
@@ -705,7 +712,7 @@ AggFn pick_agg(AggShape s, bool far = false) {
 }
 
 using FwdFn = void (*)(const int*, const int*, const float*, const int*, int, const float*, int, int, const float*,
-                       int, float*, int, int, int);
+                       int, float*, int, int, int, const EpiPack);
 template <bool AGG, int RPT>
 FwdFn pick_fwd_rpt(AggShape s) {
 #define M(L, V) if (s.lpr == L && s.vpl == V) return k_fwd_gemm<L, V, AGG, RPT>;
@@ -719,7 +726,7 @@ FwdFn pick_fwd(AggShape s, int rpt) {
 }
 
 using BwdFn = void (*)(const int*, const int*, const float*, const int*, int, const float*, int, int, const float*,
-                       int, int, const float*, float*, int, int, float*, int);
+                       int, int, const float*, float*, int, int, float*, int, const EpiPack);
 template <int IPT, bool GP, int RPT>
 BwdFn pick_bwd_t(AggShape s) {
 #define M(L, V) if (s.lpr == L && s.vpl == V) return k_bwd<L, V, IPT, GP, RPT>;
@@ -776,17 +783,17 @@ int bwd_plan(int n_rows, int d_prev, int d_k, bool with_gp, BwdPlan* out) {
 int launch_bwd_epilogue(const float* agg, int ldagg, int d_k, const float* h_prev, int ldhp, int d_prev,
                         const float* w, float* g_prev, int ldgp, int act, const int32_t* rows, int n_rows,
                         float* dw_partials, const BwdPlan& plan, cudaStream_t st, const uint32_t* hbits = nullptr,
-                        int ld_hbits = 0) {
+                        int ld_hbits = 0, const EpiPack& pk = EpiPack{}) {
   if (dw_tc_applies(d_prev, d_k) && (!g_prev || dense_tc_applies(d_k, d_prev))) {
     if (g_prev) {
       if (int rc = launch_dense_tc(agg, ldagg, rows, n_rows, d_k, nullptr, d_prev, g_prev, ldgp, act, st, w,
-                                   round4(d_k), h_prev, ldhp, hbits, ld_hbits))
+                                   round4(d_k), h_prev, ldhp, hbits, ld_hbits, nullptr, 0, &pk))
         return rc;
     }
     return launch_dw_tc(h_prev, ldhp, d_prev, agg, ldagg, d_k, rows, n_rows, dw_partials, plan.grid, st);
   }
   plan.fn<<<plan.grid, NT, plan.smem, st>>>(nullptr, nullptr, nullptr, rows, n_rows, agg, ldagg, d_k, h_prev, ldhp,
-                                            d_prev, w, g_prev, ldgp, act, dw_partials, plan.T);
+                                            d_prev, w, g_prev, ldgp, act, dw_partials, plan.T, pk);
   GCNB_AFTER_LAUNCH("bwd layer (dense epilogue)");
   return GCNB_OK;
 }
@@ -827,7 +834,8 @@ int launch_agg(const int32_t* row_ptr, const int32_t* col, const float* val, con
 
 int launch_fwd_gemm(bool agg, const int32_t* row_ptr, const int32_t* col, const float* val, const int32_t* rows,
                     int32_t n_rows, const float* x, int32_t ldx, int32_t d_in, const float* w, int32_t d_out,
-                    float* h, int32_t ldh, int32_t act, cudaStream_t st, const char* what) {
+                    float* h, int32_t ldh, int32_t act, cudaStream_t st, const char* what,
+                    const EpiPack& pk = EpiPack{}) {
   const AggShape s = agg_shape(d_in);
   int rpt = 0;
   const int T = tile_rows(d_out, s.lpr, &rpt);
@@ -837,7 +845,7 @@ int launch_fwd_gemm(bool agg, const int32_t* row_ptr, const int32_t* col, const 
       sizeof(float) * ((w ? (size_t)round4(d_in) * round4(d_out) : 0) + (size_t)T * (round4(d_in) + 4));
   GCNB_REQUIRE(smem <= 227 * 1024, "%s: tile does not fit shared memory", what);
   const int grid = occupancy_grid(reinterpret_cast<const void*>(fn), smem, (n_rows + T - 1) / T);
-  fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, x, ldx, d_in, w, d_out, h, ldh, act, T);
+  fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, x, ldx, d_in, w, d_out, h, ldh, act, T, pk);
   GCNB_AFTER_LAUNCH(what);
   return GCNB_OK;
 }
@@ -978,7 +986,7 @@ extern "C" int gcnb_bwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
                                dw_partials, plan, st);
   }
   plan.fn<<<plan.grid, NT, plan.smem, st>>>(row_ptr, col, val, rows, n_rows, g, ldg, d_k, h_prev, ldhp, d_prev, w,
-                                            g_prev, ldgp, act, dw_partials, plan.T);
+                                            g_prev, ldgp, act, dw_partials, plan.T, EpiPack{});
   GCNB_AFTER_LAUNCH("bwd layer");
   return GCNB_OK;
 }
@@ -998,7 +1006,7 @@ extern "C" int gcnb_dw_f32(const float* x, int32_t ldx, int32_t d_prev, const fl
     return launch_dw_tc(x, ldx, d_prev, a, lda, d_k, rows, n_rows, dw_partials, plan.grid, st);
   // SIMT: the backward kernel without CSR reads A's rows directly as its aggregated tile
   plan.fn<<<plan.grid, NT, plan.smem, st>>>(nullptr, nullptr, nullptr, rows, n_rows, a, lda, d_k, x, ldx, d_prev,
-                                            nullptr, nullptr, 0, GCNB_ACT_IDENTITY, dw_partials, plan.T);
+                                            nullptr, nullptr, 0, GCNB_ACT_IDENTITY, dw_partials, plan.T, EpiPack{});
   GCNB_AFTER_LAUNCH("dw");
   return GCNB_OK;
 }
@@ -1062,4 +1070,120 @@ extern "C" int gcnb_reduce_sgd_f32(const float* partials, int32_t n_slots, int64
 extern "C" int gcnb_reduce_partials_f32(const float* partials, int32_t n_slots, int64_t size, float* out,
                                         int32_t accumulate, void* stream) {
   return gcnb_reduce_sgd_f32(partials, n_slots, size, out, accumulate, nullptr, 0.0f, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Producers with the halo pack fused into their epilogue (epipack.cuh).
+
+namespace {
+int pack_of(const gcnb_halo_pack* hp, int ld_out, EpiPack* pk, const char* what) {
+  if (!hp || hp->n_seg == 0) {
+    *pk = EpiPack{};
+    return GCNB_OK;
+  }
+  GCNB_REQUIRE(hp->ldd >= ld_out, "%s: halo stride %d below the row stride %d", what, hp->ldd, ld_out);
+  return make_epipack(pk, hp->map_ptr, hp->map, hp->dst, hp->flags, hp->n_seg, hp->ldd, hp->counter);
+}
+}  // namespace
+
+extern "C" int gcnb_dense_pack_f32(const float* x, int32_t ldx, int32_t n_rows, int32_t d_in, const float* w,
+                                   int32_t d_out, float* y, int32_t ldy, int32_t act, uint32_t* bits,
+                                   int32_t ld_bits, const gcnb_halo_pack* pack, void* stream) {
+  GCNB_REQUIRE(n_rows >= 0, "dense pack: n_rows must be >= 0");
+  GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "dense pack: unknown activation %d", act);
+  GCNB_REQUIRE(d_in >= 1 && d_in <= 256 && d_out >= 1 && d_out <= 256, "dense pack: widths out of range");
+  GCNB_REQUIRE(ldx % 4 == 0 && ldy % 4 == 0 && ldx >= round4(d_in) && ldy >= round4(d_out),
+               "dense pack: row strides must be multiples of 4 and cover the widths");
+  GCNB_REQUIRE(x && w && y && aligned16(x) && aligned16(w) && aligned16(y),
+               "dense pack: operands must be 16-byte aligned");
+  GCNB_REQUIRE(!bits || (act == GCNB_ACT_RELU && ld_bits % 4 == 0 && ld_bits * 32 >= d_out && aligned16(bits) &&
+                         dense_tc_applies(d_in, d_out)),
+               "dense pack: sign bits need a ReLU tcgen05 transform and a stride of >= d_out/32 words");
+  EpiPack pk;
+  if (int rc = pack_of(pack, ldy, &pk, "dense pack")) return rc;
+  if (n_rows == 0) return GCNB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dense_tc_applies(d_in, d_out))
+    return launch_dense_tc(x, ldx, nullptr, n_rows, d_in, w, d_out, y, ldy, act, st, nullptr, 0, nullptr, 0, nullptr,
+                           0, bits, ld_bits, &pk);
+  if (dense_blocked_applies(d_in, d_out))
+    return launch_dense_blocked(x, ldx, nullptr, n_rows, d_in, w, d_out, y, ldy, act, st, &pk);
+  return launch_fwd_gemm(false, nullptr, nullptr, nullptr, nullptr, n_rows, x, ldx, d_in, w, d_out, y, ldy, act, st,
+                         "dense pack", pk);
+}
+
+extern "C" int gcnb_fwd_layer_pack_f32(const int32_t* row_ptr, const int32_t* col, const float* val, int32_t n_rows,
+                                       const float* x, int32_t ldx, int32_t d_in, const float* w, int32_t d_out,
+                                       float* h, int32_t ldh, int32_t act, const gcnb_halo_pack* pack,
+                                       void* stream) {
+  if (int rc = check_csr_args(row_ptr, col, val, n_rows)) return rc;
+  GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "fwd layer pack: unknown activation %d", act);
+  GCNB_REQUIRE(d_in >= 1 && d_in <= 256 && d_out >= 1 && d_out <= 256, "fwd layer pack: widths out of range");
+  GCNB_REQUIRE(w != nullptr, "fwd layer pack: the fused form needs W (aggregate-only layers pack separately)");
+  GCNB_REQUIRE(ldx % 4 == 0 && ldh % 4 == 0 && ldx >= round4(d_in) && ldh >= round4(d_out),
+               "fwd layer pack: row strides must be multiples of 4 and cover the widths");
+  GCNB_REQUIRE(aligned16(x) && aligned16(h) && aligned16(w), "fwd layer pack: operands must be 16-byte aligned");
+  EpiPack pk;
+  if (int rc = pack_of(pack, ldh, &pk, "fwd layer pack")) return rc;
+  if (n_rows == 0) return GCNB_OK;
+  return launch_fwd_gemm(true, row_ptr, col, val, nullptr, n_rows, x, ldx, d_in, w, d_out, h, ldh, act,
+                         (cudaStream_t)stream, "fwd layer pack (aggregate+transform)", pk);
+}
+
+extern "C" int gcnb_bwd_layer_pack_f32(const int32_t* row_ptr, const int32_t* col, const float* val, int32_t n_rows,
+                                       const float* g, int32_t ldg, int32_t d_k, const float* h_prev, int32_t ldhp,
+                                       int32_t d_prev, const float* w, float* g_prev, int32_t ldgp, int32_t act,
+                                       float* dw_partials, float* workspace, const gcnb_halo_pack* pack,
+                                       void* stream) {
+  if (int rc = check_csr_args(row_ptr, col, val, n_rows)) return rc;
+  GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "bwd layer pack: unknown activation %d", act);
+  GCNB_REQUIRE(d_prev >= 1 && d_prev <= 256 && d_k >= 1 && d_k <= 256, "bwd layer pack: widths out of range");
+  GCNB_REQUIRE(ldg % 4 == 0 && ldhp % 4 == 0 && ldg >= round4(d_k) && ldhp >= round4(d_prev),
+               "bwd layer pack: row strides must be multiples of 4 and cover the widths");
+  GCNB_REQUIRE(g_prev && w && ldgp % 4 == 0 && ldgp >= round4(d_prev) && aligned16(g_prev) && aligned16(w),
+               "bwd layer pack: the packed G_prev needs W and an aligned stride >= round4(d_prev)");
+  GCNB_REQUIRE(g && h_prev && dw_partials && aligned16(g) && aligned16(h_prev) && aligned16(dw_partials),
+               "bwd layer pack: operands must be non-null and 16-byte aligned");
+  GCNB_REQUIRE(!workspace || aligned16(workspace), "bwd layer pack: workspace must be 16-byte aligned");
+  EpiPack pk;
+  if (int rc = pack_of(pack, ldgp, &pk, "bwd layer pack")) return rc;
+  BwdPlan plan;
+  if (int rc = bwd_plan(n_rows, d_prev, d_k, true, &plan)) return rc;
+  if (n_rows == 0) return GCNB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (workspace && bwd_split(d_prev, d_k)) {
+    if (int rc = launch_agg(row_ptr, col, val, nullptr, n_rows, g, ldg, d_k, workspace, round4(d_k), -1, st,
+                            "bwd layer pack (aggregate)"))
+      return rc;
+    return launch_bwd_epilogue(workspace, round4(d_k), d_k, h_prev, ldhp, d_prev, w, g_prev, ldgp, act, nullptr,
+                               n_rows, dw_partials, plan, st, nullptr, 0, pk);
+  }
+  plan.fn<<<plan.grid, NT, plan.smem, st>>>(row_ptr, col, val, nullptr, n_rows, g, ldg, d_k, h_prev, ldhp, d_prev, w,
+                                            g_prev, ldgp, act, dw_partials, plan.T, pk);
+  GCNB_AFTER_LAUNCH("bwd layer pack");
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_bwd_epilogue_pack_f32(const float* agg, int32_t ldagg, int32_t d_k, const float* h_prev,
+                                          int32_t ldhp, int32_t d_prev, const float* w, float* g_prev, int32_t ldgp,
+                                          int32_t act, const uint32_t* hbits, int32_t ld_hbits, int32_t n_rows,
+                                          float* dw_partials, const gcnb_halo_pack* pack, void* stream) {
+  GCNB_REQUIRE(!hbits || (ld_hbits % 4 == 0 && ld_hbits * 32 >= d_prev && aligned16(hbits)),
+               "bwd epilogue pack: sign-bit rows need a stride of >= d_prev/32 words, a multiple of 4");
+  GCNB_REQUIRE(n_rows >= 0, "bwd epilogue pack: n_rows must be >= 0");
+  GCNB_REQUIRE(act == GCNB_ACT_RELU || act == GCNB_ACT_IDENTITY, "bwd epilogue pack: unknown activation %d", act);
+  GCNB_REQUIRE(d_prev >= 1 && d_prev <= 256 && d_k >= 1 && d_k <= 256, "bwd epilogue pack: widths out of range");
+  GCNB_REQUIRE(ldagg % 4 == 0 && ldhp % 4 == 0 && ldagg >= round4(d_k) && ldhp >= round4(d_prev),
+               "bwd epilogue pack: row strides must be multiples of 4 and cover the widths");
+  GCNB_REQUIRE(g_prev && w && ldgp % 4 == 0 && ldgp >= round4(d_prev) && aligned16(g_prev) && aligned16(w),
+               "bwd epilogue pack: the packed G_prev needs W and an aligned stride >= round4(d_prev)");
+  GCNB_REQUIRE(agg && h_prev && dw_partials && aligned16(agg) && aligned16(h_prev) && aligned16(dw_partials),
+               "bwd epilogue pack: operands must be non-null and 16-byte aligned");
+  EpiPack pk;
+  if (int rc = pack_of(pack, ldgp, &pk, "bwd epilogue pack")) return rc;
+  BwdPlan plan;
+  if (int rc = bwd_plan(n_rows, d_prev, d_k, true, &plan)) return rc;
+  if (n_rows == 0) return GCNB_OK;
+  return launch_bwd_epilogue(agg, ldagg, d_k, h_prev, ldhp, d_prev, w, g_prev, ldgp, act, nullptr, n_rows,
+                             dw_partials, plan, (cudaStream_t)stream, hbits, ld_hbits, pk);
 }

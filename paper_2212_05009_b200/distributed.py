@@ -304,7 +304,7 @@ class DistributedTrainer:
         self.expected_ar = a.tensor("expected_ar", (p,), torch.int64)
         self.flags_bar = a.tensor("flags_bar", (p,), torch.int64)
         self.expected_bar = a.tensor("expected_bar", (p,), torch.int64)
-        self.counter = a.tensor("counter", (4,), torch.int32)
+        self.counter = a.tensor("counter", (8,), torch.int32)
         self.err = a.tensor("err", (4,), torch.int32)
         self.slot = self.off["_slot"]
         self.slots = a.tensor("slots", (2, p, self.slot), torch.float32)
@@ -388,45 +388,78 @@ class DistributedTrainer:
     def enqueue_epoch(self, parity: int, comm: bool = True) -> None:
         import torch
 
+        from .runtime import FusedPack
+
         st, L = self.st, self.st.n_layers
         cnt = self.counter.data_ptr()
         self._forked = False
+        # Halo packs fused into the producing kernel's epilogue (FusedPack):
+        # the producer stores each boundary row into the receivers' halos as
+        # it writes it and rings the doorbells at its end — no pack launch and
+        # no re-read; an exchange whose producer is not one launch over all own
+        # rows (interior/boundary halves, the windowed aggregation, H⁰) is
+        # packed on the comm stream instead.  counter[4] serves the fused
+        # producers (one at a time on the compute stream).
+        def fused(phase: str, k: int):
+            if not (comm and self.fuse_pack) or k < 1 or k > L:
+                return None
+            if phase == "bwd" and st.skips_bwd_exchange(k):
+                return None
+            bases = self.fwd_bases[k] if phase == "fwd" else self.bwd_bases[k]
+            flags = self.halo_flag_fwd if phase == "fwd" else self.halo_flag_bwd
+            return FusedPack(bases, flags, cnt + 16)
+
+        done = set()
+
+        def took(pk, phase, k):
+            if pk is not None and pk.done:
+                done.add((phase, k))
+
         for k in range(1, L + 1):
-            st.fwd_transform(k)
-            if comm:
+            pk = fused("fwd", k)
+            st.fwd_transform(k, pack=pk)
+            took(pk, "fwd", k)
+            if comm and ("fwd", k) not in done:
                 self._pack("fwd", k)
+            # H^k is the next layer's operand when that layer aggregates first
+            nxt = fused("fwd", k + 1) if k < L and not st.transform_first[k + 1] else None
             if self.overlap:
                 st.fwd_compute(k, "interior")
             if comm:
                 self._wait(self.flags_halo, self.expected_halo, self.sched.fwd_src, f"wait_fwd{k}")
-            st.fwd_compute(k, "boundary" if self.overlap else "all")
+            st.fwd_compute(k, "boundary" if self.overlap else "all", pack=None if self.overlap else nxt)
             if self.overlap:
-                st.fwd_finish(k)
+                st.fwd_finish(k, pack=nxt)
+            took(nxt, "fwd", k + 1)
         # the backward halo of layer L is packed by the loss kernel itself
         fused_L = comm and self.fuse_pack and not st.skips_bwd_exchange(L) and bool(st.layout.bwd.send_dst)
         if fused_L:
             st.loss_grad(1.0 / self.n_lab, pack=(self.bwd_bases[L], self.halo_flag_bwd, self.counter.data_ptr() + 12))
+            done.add(("bwd", L))
         else:
             st.loss_grad(1.0 / self.n_lab)
         for k in range(L, 0, -1):
             if st.skips_bwd_exchange(k):
                 st.reduce_dw(k, st.dw_from_forward(k))
                 continue
-            if comm and not (k == L and fused_L):
+            if comm and ("bwd", k) not in done:
                 self._pack("bwd", k)
+            nxt = fused("bwd", k - 1)
             if self.overlap:
                 gi = st.bwd_compute(k, "interior", slot=0)
                 if comm:
                     self._wait(self.flags_halo, self.expected_halo, self.sched.bwd_src, f"wait_bwd{k}")
                 gb = st.bwd_compute(k, "boundary", slot=gi)
                 if st.bwd_split(k):
-                    st.reduce_dw(k, st.bwd_finish(k))
+                    st.reduce_dw(k, st.bwd_finish(k, pack=nxt))
                 else:
                     st.reduce_dw(k, gi + gb)
             else:
                 if comm:
                     self._wait(self.flags_halo, self.expected_halo, self.sched.bwd_src, f"wait_bwd{k}")
-                st.reduce_dw(k, st.bwd_compute(k, "all", slot=0))
+                st.reduce_dw(k, st.bwd_compute(k, "all", slot=0, pack=nxt))
+            took(nxt, "bwd", k - 1)
+        self.fused_packs = done
         n_tot = st.n_pack + 4
         from .profiling import span
 

@@ -290,6 +290,18 @@ class _WeightList(list):
         self._st._upload_weight(k, value)
 
 
+class FusedPack:
+    """A halo exchange to fuse into the epilogue of the kernel that produces its
+    rows (gcnb_halo_pack): dst_bases[dst] = (device pointer of the receiver's
+    [own | halo] buffer, its own-row count), the receivers' doorbells and a
+    device int for the last-block election.  The producer sets `done` when it
+    took the pack; otherwise the caller packs separately."""
+
+    def __init__(self, dst_bases: dict, flags, counter: int):
+        self.dst_bases, self.flags, self.counter = dst_bases, flags, counter
+        self.done = False
+
+
 class ProcState:
     """Everything one rank stores, resident on its CUDA device (runtime.py:160-189).
 
@@ -558,18 +570,40 @@ class ProcState:
         """(tensor, width) that layer k aggregates and exchanges."""
         return self.xext[k], (self.dims[k] if self.transform_first[k] else self.dims[k - 1])
 
-    def fwd_transform(self, k: int) -> None:
-        """T^k = H^{k-1}·W^k into the own rows of the layer-k operand."""
+    def _halo_pack(self, phase: str, pack: FusedPack, ld: int):
+        """(gcnb_halo_pack reference, objects to keep alive, packed floats) for the
+        phase's send lists, or None when this rank sends nothing."""
+        lay = self.layout.fwd if phase == "fwd" else self.layout.bwd
+        if pack is None or not lay.send_dst or self.n_own == 0:
+            return None
+        dsts = [pack.dst_bases[dst][0] + (pack.dst_bases[dst][1] + slot) * ld * 4
+                for dst, slot in zip(lay.send_dst, lay.dst_slot)]
+        mp, mm = self.send_map(phase)
+        ref, keep = _lib.halo_pack(mp.data_ptr(), mm.data_ptr(), dsts, pack.flags, ld, pack.counter)
+        return ref, (keep, mp, mm), 4 * ld * int(lay.send_ptr[-1])
+
+    def fwd_transform(self, k: int, pack: FusedPack | None = None) -> None:
+        """T^k = H^{k-1}·W^k into the own rows of the layer-k operand (pack: the
+        layer-k forward halo stored into the receivers as the rows are made)."""
         if not self.transform_first[k] or self.n_own == 0:
             return
         x = self.hbuf[k - 1]
         n, a, b = self.n_own, self.dims[k - 1], self.dims[k]
-        with span(f"dense{k}", 4 * (n * a + a * b + n * b), 2 * n * a * b, self.stream()):
-            _lib.call("gcnb_dense_f32", x.data_ptr(), x.shape[1], None, n, a, self.w[k].data_ptr(), b,
-                      self.xext[k].data_ptr(), self.xext[k].shape[1], _lib.ACT["identity"], self.stream())
+        y = self.xext[k]
+        hp = self._halo_pack("fwd", pack, y.shape[1])
+        with span(f"dense{k}", 4 * (n * a + a * b + n * b) + (hp[2] if hp else 0), 2 * n * a * b, self.stream()):
+            if hp is None:
+                _lib.call("gcnb_dense_f32", x.data_ptr(), x.shape[1], None, n, a, self.w[k].data_ptr(), b,
+                          y.data_ptr(), y.shape[1], _lib.ACT["identity"], self.stream())
+            else:
+                _lib.call("gcnb_dense_pack_f32", x.data_ptr(), x.shape[1], n, a, self.w[k].data_ptr(), b,
+                          y.data_ptr(), y.shape[1], _lib.ACT["identity"], None, 0, hp[0], self.stream())
+                pack.done = True
 
-    def fwd_compute(self, k: int, rows: str = "all") -> None:
-        """runtime._fwd_compute for the selected own rows (all | interior | boundary)."""
+    def fwd_compute(self, k: int, rows: str = "all", pack: FusedPack | None = None) -> None:
+        """runtime._fwd_compute for the selected own rows (all | interior | boundary).
+        pack (rows == "all"): the forward halo of layer k+1 (H^k), fused into
+        the kernel that writes H^k where that is one launch over all own rows."""
         op = self.op_fwd
         sel, n_sel = self._rows(op, rows)
         if n_sel == 0:
@@ -595,7 +629,7 @@ class ProcState:
                               op.csr.val.data_ptr(), sel, n_sel, x.data_ptr(), x.shape[1], width, 0, width,
                               ws.data_ptr(), ws.shape[1], _lib.ACT["identity"], self.stream())
             if rows == "all":
-                self.fwd_finish(k)
+                self.fwd_finish(k, pack)
             return
         algo = 4 * (n_sel + 1) + 8 * nnz + 4 * width * nnz + 4 * d_out * n_sel
         flops = 2 * nnz * width
@@ -607,6 +641,13 @@ class ProcState:
             if not fused and op.use_window(rows, width):
                 op.aggregate_all(x, width, h, self.act, self.stream())
                 return
+            hp = self._halo_pack("fwd", pack, h.shape[1]) if fused and rows == "all" else None
+            if hp is not None:
+                _lib.call("gcnb_fwd_layer_pack_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
+                          op.csr.val.data_ptr(), n_sel, x.data_ptr(), x.shape[1], width, w, d_out, h.data_ptr(),
+                          h.shape[1], self.act, hp[0], self.stream())
+                pack.done = True
+                return
             _lib.call("gcnb_fwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
                       op.csr.val.data_ptr(), sel, n_sel, x.data_ptr(), x.shape[1], width, w, d_out, h.data_ptr(),
                       h.shape[1], self.act, self.stream())
@@ -615,16 +656,24 @@ class ProcState:
         """Layer k's forward runs as aggregation + dense transform (fwd_finish)."""
         return not self.transform_first[k] and self.fwd_ws[k] is not None
 
-    def fwd_finish(self, k: int) -> None:
-        """Dense transform H^k = act(Y·W^k) of all own rows from the workspace."""
+    def fwd_finish(self, k: int, pack: FusedPack | None = None) -> None:
+        """Dense transform H^k = act(Y·W^k) of all own rows from the workspace
+        (pack: the forward halo of layer k+1 fused into it)."""
         if not self.fwd_split(k) or self.n_own == 0:
             return
         ws, h = self.fwd_ws[k], self.hbuf[k]
         n, width, d_out = self.n_own, self.dims[k - 1], self.dims[k]
         bits = self.hbits[k]
         self.hbits_valid[k] = bits is not None and _lib.dense_tc_applies(width, d_out)
-        with span(f"dense{k}", 4 * (n * width + width * d_out + n * d_out), 2 * n * width * d_out, self.stream()):
-            if self.hbits_valid[k]:
+        hp = self._halo_pack("fwd", pack, h.shape[1])
+        with span(f"dense{k}", 4 * (n * width + width * d_out + n * d_out) + (hp[2] if hp else 0),
+                  2 * n * width * d_out, self.stream()):
+            if hp is not None:
+                _lib.call("gcnb_dense_pack_f32", ws.data_ptr(), ws.shape[1], n, width, self.w[k].data_ptr(), d_out,
+                          h.data_ptr(), h.shape[1], self.act, bits.data_ptr() if self.hbits_valid[k] else None,
+                          bits.shape[1] if self.hbits_valid[k] else 0, hp[0], self.stream())
+                pack.done = True
+            elif self.hbits_valid[k]:
                 _lib.call("gcnb_dense_bits_f32", ws.data_ptr(), ws.shape[1], n, width, self.w[k].data_ptr(), d_out,
                           h.data_ptr(), h.shape[1], bits.data_ptr(), bits.shape[1], self.stream())
             else:
@@ -635,9 +684,10 @@ class ProcState:
         """Layer k's backward runs as aggregation + dense epilogue (bwd_finish)."""
         return self.bwd_ws[k] is not None
 
-    def bwd_finish(self, k: int) -> int:
+    def bwd_finish(self, k: int, pack: FusedPack | None = None) -> int:
         """G^{k-1} and the ΔW^k partials of all own rows from the aggregate in the
-        workspace (after interior/boundary aggregations); returns slots used."""
+        workspace (after interior/boundary aggregations); returns slots used.
+        pack: the backward halo of layer k-1 (G^{k-1}) fused into the epilogue."""
         ws = self.bwd_ws[k]
         hp = self.hbuf[k - 1]
         gp = self.gext[k - 1] if k > 1 else None
@@ -649,7 +699,16 @@ class ProcState:
         bits = self.hbits[k - 1] if gp is not None and self.hbits_valid[k - 1] else None
         mask_bytes = (4 * n * bits.shape[1] if bits is not None else 4 * dp * n) if gp is not None else 0
         algo = 4 * n * (dk + dp) + 4 * dp * dk * used + mask_bytes + (4 * dp * n if gp is not None else 0)
-        with span(f"bwd{k}_dense", algo, 2 * n * dp * dk * (2 if gp is not None else 1), self.stream()):
+        hpk = self._halo_pack("bwd", pack, gp.shape[1]) if gp is not None else None
+        with span(f"bwd{k}_dense", algo + (hpk[2] if hpk else 0), 2 * n * dp * dk * (2 if gp is not None else 1),
+                  self.stream()):
+            if hpk is not None:
+                _lib.call("gcnb_bwd_epilogue_pack_f32", ws.data_ptr(), ws.shape[1], dk, hp.data_ptr(), hp.shape[1],
+                          dp, self.w[k].data_ptr(), gp.data_ptr(), gp.shape[1], self.act,
+                          None if bits is None else bits.data_ptr(), 0 if bits is None else bits.shape[1], n,
+                          self.partials[k].data_ptr(), hpk[0], self.stream())
+                pack.done = True
+                return used
             _lib.call("gcnb_bwd_epilogue_f32", ws.data_ptr(), ws.shape[1], dk, hp.data_ptr(), hp.shape[1], dp,
                       self.w[k].data_ptr(), 0 if gp is None else gp.data_ptr(), 0 if gp is None else gp.shape[1],
                       self.act, None if bits is None else bits.data_ptr(), 0 if bits is None else bits.shape[1],
@@ -700,8 +759,10 @@ class ProcState:
                       self.loss_sum.data_ptr(), mp.data_ptr(), mm.data_ptr(), _lib.ptr_array(dsts),
                       _lib.ptr_array(flags), len(dsts), ld, counter, self.stream())
 
-    def bwd_compute(self, k: int, rows: str = "all", slot: int = 0) -> int:
-        """runtime._bwd_compute: G^{k-1} (k > 1) and ΔW^k partials; returns slots used."""
+    def bwd_compute(self, k: int, rows: str = "all", slot: int = 0, pack: FusedPack | None = None) -> int:
+        """runtime._bwd_compute: G^{k-1} (k > 1) and ΔW^k partials; returns slots used.
+        pack (rows == "all"): the backward halo of layer k-1 fused into the
+        kernel that writes G^{k-1}."""
         op = self.op_bwd
         if k == self.n_layers and getattr(self, "op_bwd_lab", None) is not None:
             op = self.op_bwd_lab  # G^L is zero off the labelled rows: only labelled columns
@@ -727,7 +788,7 @@ class ProcState:
                     _lib.call("gcnb_spmm_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
                               op.csr.val.data_ptr(), sel, n_sel, g.data_ptr(), g.shape[1], self.dims[k],
                               ws.data_ptr(), ws.shape[1], self.stream())
-            return self.bwd_finish(k) if rows == "all" else 0
+            return self.bwd_finish(k, pack) if rows == "all" else 0
         hp = self.hbuf[k - 1]
         gp = self.gext[k - 1] if k > 1 else None
         part = self.partials[k][slot:]
@@ -741,7 +802,15 @@ class ProcState:
         comp = op.compulsory(rows, dk, 0) + 4 * dp * n_sel + 4 * dp * dk * used
         if gp is not None:
             comp += 4 * dp * n_sel + 4 * dp * dk
-        with span(f"bwd{k}", algo, flops, self.stream(), comp):
+        hpk = self._halo_pack("bwd", pack, gp.shape[1]) if gp is not None and rows == "all" else None
+        with span(f"bwd{k}", algo + (hpk[2] if hpk else 0), flops, self.stream(), comp):
+            if hpk is not None:
+                _lib.call("gcnb_bwd_layer_pack_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
+                          op.csr.val.data_ptr(), n_sel, g.data_ptr(), g.shape[1], dk, hp.data_ptr(), hp.shape[1], dp,
+                          self.w[k].data_ptr(), gp.data_ptr(), gp.shape[1], self.act, part.data_ptr(),
+                          0 if self.bwd_ws[k] is None else self.bwd_ws[k].data_ptr(), hpk[0], self.stream())
+                pack.done = True
+                return used
             _lib.call("gcnb_bwd_layer_f32", op.csr.row_ptr.data_ptr(), op.csr.col.data_ptr(),
                       op.csr.val.data_ptr(), sel, n_sel, g.data_ptr(), g.shape[1], dk, hp.data_ptr(), hp.shape[1],
                       dp, self.w[k].data_ptr(), 0 if gp is None else gp.data_ptr(),

@@ -8,6 +8,7 @@ oracle restatement of the reference's round scheduler (oracle/, test
 infrastructure) and prints one JSON line.  Exit code 1 on mismatch.
 """
 import argparse
+import hashlib
 import json
 import os
 import sys
@@ -64,7 +65,9 @@ def main():
     gathered = [None] * world
     dist.all_gather_object(gathered, [w.tolist() for w in ws])
     ok = True
-    report = {"world": world, "directed": args.directed, "graph": args.graph, "reuse": args.reuse, "losses": losses}
+    report = {"world": world, "directed": args.directed, "graph": args.graph, "reuse": args.reuse, "losses": losses,
+              "fused_packs": [f"{ph}{k}" for ph, k in sorted(tr.fused_packs)],
+              "weights_sha": hashlib.sha256(b"".join(np.ascontiguousarray(w).tobytes() for w in ws)).hexdigest()}
     if rank == 0:
         w_ref, l_ref, words, _ = o.parallel_train(o.as_csr(a_hat), h0, pi.assignment, world, list(model.weights),
                                                   ids, y, args.epochs, directed=args.directed)
