@@ -40,10 +40,13 @@ __device__ __forceinline__ void epi_store(const EpiPack& pk, int row, int ch, fl
 
 // The rows this block produced — tiles blockIdx.x, blockIdx.x + gridDim.x, ...
 // of T row positions; position i is own row rows[i] (rows == nullptr: i) —
-// stored into their receiver slots after the fact: one warp per row, lanes
-// over the c4 float4 chunks, re-read (plain loads: written by this kernel, visible after the barrier).
-// Keeps the pack out of the producer's register-tight main loop.  All threads
-// call it after the block's last store of Y and a __syncthreads.
+// stored into their receiver slots after the fact, which keeps the pack out of
+// the producer's register-tight main loop.  A warp tests 32 rows per step (one
+// coalesced map_ptr load per lane, a ballot), then spreads the (boundary row,
+// float4 chunk) pairs of those rows over its lanes, 32 independent copies per
+// round (plain loads: the rows were written by this block, visible after its
+// barrier).  All
+// threads call it after the block's last store of Y and a __syncthreads.
 __device__ __forceinline__ void epi_forward(const EpiPack& pk, const float* Y, int ldy, const int* rows, int n_rows,
                                             int T, int c4) {
   if (!pk.map_ptr) return;
@@ -51,16 +54,29 @@ __device__ __forceinline__ void epi_forward(const EpiPack& pk, const float* Y, i
   const int n_tiles = (n_rows + T - 1) / T;
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int t1 = min(n_rows, (tile + 1) * T);
-    for (int i = tile * T + warp; i < t1; i += nw) {
-      const int row = rows ? __ldg(rows + i) : i;
-      const int e0 = __ldg(pk.map_ptr + row), e1 = __ldg(pk.map_ptr + row + 1);
-      if (e0 == e1) continue;
-      const float4* y = reinterpret_cast<const float4*>(Y + (size_t)row * ldy);
-      for (int ch = lane; ch < c4; ch += 32) {
-        const float4 v = y[ch];
-        for (int e = e0; e < e1; ++e) {
-          const int2 m = __ldg(pk.map + e);
-          pk.dst[m.x][(size_t)m.y * pk.ldd4 + ch] = v;
+    for (int i0 = tile * T + warp * 32; i0 < t1; i0 += nw * 32) {
+      const int i = i0 + lane;
+      int row = 0, e0 = 0, e1 = 0;
+      if (i < t1) {
+        row = rows ? __ldg(rows + i) : i;
+        e0 = __ldg(pk.map_ptr + row);
+        e1 = __ldg(pk.map_ptr + row + 1);
+      }
+      const unsigned todo = __ballot_sync(0xffffffffu, e1 > e0);
+      const int items = __popc(todo) * c4;  // (boundary row, chunk) pairs, spread over the lanes
+      for (int base = 0; base < items; base += 32) {
+        const int idx = base + lane;
+        const int k = idx / c4, ch = idx - k * c4;
+        const int src = idx < items ? (int)__fns(todo, 0, k + 1) : 0;
+        const int r = __shfl_sync(0xffffffffu, row, src);
+        const int a = __shfl_sync(0xffffffffu, e0, src);
+        const int b = __shfl_sync(0xffffffffu, e1, src);
+        if (idx < items) {
+          const float4 v = reinterpret_cast<const float4*>(Y + (size_t)r * ldy)[ch];
+          for (int e = a; e < b; ++e) {
+            const int2 m = __ldg(pk.map + e);
+            pk.dst[m.x][(size_t)m.y * pk.ldd4 + ch] = v;
+          }
         }
       }
     }

@@ -345,11 +345,12 @@ class DistributedTrainer:
         # halo packs run on their own stream, concurrent with the interior
         # aggregation of the compute stream (joined back once per epoch)
         self.comm_stream = torch.cuda.Stream(device)
-        # fuse the halo pack into producing kernels where one exists (the loss
-        # kernel for the last layer's backward exchange); GCNB_FUSE_PACK=0: separate k_pack
+        # fuse the halo pack into producing kernels where one exists (FusedPack:
+        # see enqueue_epoch); GCNB_FUSE_PACK=0: separate k_pack launches
         self.fuse_pack = os.environ.get("GCNB_FUSE_PACK", "1") != "0"
         if self.fuse_pack:
-            self.st.send_map("bwd")  # device arrays built now, never inside a graph capture
+            self.st.send_map("fwd")  # device arrays built now, never inside a graph capture
+            self.st.send_map("bwd")
         torch.cuda.synchronize(device)
         dist.barrier()
         self.graphs = {}

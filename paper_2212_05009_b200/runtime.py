@@ -978,56 +978,151 @@ def _log_phase(states, net, phase: str, k: int, epoch: int, step: int) -> None:
                                             nbytes=rows * devmem.ld_of(width) * 4))
 
 
-def _forward(states, net, epoch: int, step: int) -> None:
+class _RankStreams:
+    """The "threads" scheduler on one device (runtime.py:386-440): every rank
+    runs its step functions on its own CUDA stream, a message is an event the
+    sender records after its pack and the receiver's stream waits on before
+    the compute that reads the halo (SimNetwork.recv), and allreduce_sum is a
+    join of all rank streams into the caller's stream, the rank-ordered sum,
+    and a fork back (the barrier).  Ranks overlap on the GPU wherever the
+    dependencies allow; every kernel and its inputs are those of the round
+    order, so results are bit-identical to it."""
+
+    def __init__(self, states):
+        self.dev = states[0].device
+        self.cur = torch.cuda.current_stream(self.dev)
+        self.streams = []
+        for st in states:
+            if getattr(st, "_rank_stream", None) is None:
+                st._rank_stream = torch.cuda.Stream(self.dev)
+            self.streams.append(st._rank_stream)
+        self.sent = {}
+        self.fork()
+
+    def on(self, i: int):
+        return torch.cuda.stream(self.streams[i])
+
+    def fork(self) -> None:
+        ev = torch.cuda.Event()
+        ev.record(self.cur)
+        for s in self.streams:
+            s.wait_event(ev)
+
+    def join(self) -> None:
+        for s in self.streams:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            self.cur.wait_event(ev)
+
+    def send(self, i: int, rank: int) -> None:
+        ev = torch.cuda.Event()
+        ev.record(self.streams[i])
+        self.sent[rank] = ev
+
+    def recv(self, i: int, srcs) -> None:
+        for src in srcs:
+            self.streams[i].wait_event(self.sent[int(src)])
+
+
+def _on(rs, i: int):
+    return rs.on(i) if rs is not None else _NULLCTX
+
+
+class _NullCtx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NULLCTX = _NullCtx()
+
+
+def _forward(states, net, epoch: int, step: int, rs: _RankStreams | None = None) -> None:
     L = states[0].n_layers
     for k in range(1, L + 1):
-        for st in states:
-            st.fwd_transform(k)
+        for i, st in enumerate(states):
+            with _on(rs, i):
+                st.fwd_transform(k)
         bases = _bases(states, "fwd", k)
-        for st in states:
-            st.pack_to("fwd", k, bases)
+        for i, st in enumerate(states):
+            with _on(rs, i):
+                st.pack_to("fwd", k, bases)
+                if rs is not None:
+                    rs.send(i, st.rank)
         _log_phase(states, net, "fwd", k, epoch, step)
-        for st in states:
-            st.fwd_compute(k, "all")
+        for i, st in enumerate(states):
+            with _on(rs, i):
+                if rs is not None:
+                    rs.recv(i, st.layout.fwd.recv_from)
+                st.fwd_compute(k, "all")
+    if rs is not None:
+        rs.join()
     for st in states:
         st._has_trace = True
 
 
-def _backward(states, net, n_labeled: int, epoch: int, step: int, loss_out: torch.Tensor | None) -> None:
+def _backward(states, net, n_labeled: int, epoch: int, step: int, loss_out: torch.Tensor | None,
+              rs: _RankStreams | None = None) -> None:
     L = states[0].n_layers
     inv = 1.0 / n_labeled if n_labeled else 0.0
-    for st in states:
-        st.loss_grad(inv)
+    if rs is not None:
+        rs.fork()
+    for i, st in enumerate(states):
+        with _on(rs, i):
+            st.loss_grad(inv)
     if loss_out is not None:
+        if rs is not None:
+            rs.join()
         _lib.call("gcnb_sum_buffers_f64", _lib.ptr_array([st.loss_sum.data_ptr() for st in states]), len(states), 1,
-                  loss_out.data_ptr(), states[0].stream())
+                  loss_out.data_ptr(), torch.cuda.current_stream(states[0].device).cuda_stream)
     for k in range(L, 0, -1):
         skip = states[0].skips_bwd_exchange(k)
         if not skip:
             bases = _bases(states, "bwd", k)
-            for st in states:
-                st.pack_to("bwd", k, bases)
+            for i, st in enumerate(states):
+                with _on(rs, i):
+                    st.pack_to("bwd", k, bases)
+                    if rs is not None:
+                        rs.send(i, st.rank)
             _log_phase(states, net, "bwd", k, epoch, step)
         if len(states) == 1:
             # one rank: the ΔW reduction and the SGD step are one kernel
             st = states[0]
-            used = st.dw_from_forward(k) if skip else st.bwd_compute(k, "all")
-            st.reduce_dw(k, used, apply_sgd=True)
+            with _on(rs, 0):
+                used = st.dw_from_forward(k) if skip else st.bwd_compute(k, "all")
+                st.reduce_dw(k, used, apply_sgd=True)
             st.dw_total[k] = st.dw[k]
             continue
-        for st in states:
-            used = st.dw_from_forward(k) if skip else st.bwd_compute(k, "all")
-            st.reduce_dw(k, used)
+        for i, st in enumerate(states):
+            with _on(rs, i):
+                if rs is not None and not skip:
+                    rs.recv(i, st.layout.bwd.recv_from)
+                used = st.dw_from_forward(k) if skip else st.bwd_compute(k, "all")
+                st.reduce_dw(k, used)
         # allreduce_sum of ΔW^k in ascending rank order, then SGD on every replica.
         # Updating W^k right after its layer is exact: no later (lower) layer reads W^k.
+        if rs is not None:
+            rs.join()
         total = states[0].dw_sum[k]
         _lib.call("gcnb_sum_buffers_f32", _lib.ptr_array([st.dw[k].data_ptr() for st in states]), len(states),
-                  total.numel(), total.data_ptr(), states[0].stream())
-        for st in states:
-            st.dw_total[k] = total
-            st.sgd(k, total)
+                  total.numel(), total.data_ptr(), torch.cuda.current_stream(states[0].device).cuda_stream)
+        if rs is not None:
+            rs.fork()
+        for i, st in enumerate(states):
+            with _on(rs, i):
+                st.dw_total[k] = total
+                st.sgd(k, total)
+    if rs is not None:
+        rs.join()
     for st in states:
         st._has_grad = True
+
+
+def _streams_for(states, scheduler: str):
+    """Per-rank streams for the "threads" scheduler (None: the round order)."""
+    return _RankStreams(states) if scheduler == "threads" and len(states) > 1 else None
 
 
 class EpochRunner:
@@ -1114,7 +1209,7 @@ def parallel_feedforward(states, net, scheduler: str = "round", epoch: int = 0):
     _check_scheduler(scheduler)
     _check_device(states)
     with torch.cuda.device(states[0].device):
-        _forward(states, net, epoch, 0)
+        _forward(states, net, epoch, 0, _streams_for(states, scheduler))
     return states
 
 
@@ -1134,7 +1229,7 @@ def parallel_backprop(states, net, labels, scheduler: str = "round", epoch: int 
         loss = torch.zeros(1, dtype=torch.float64, device=dev)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        _backward(states, net, n_lab, epoch, 0, loss)
+        _backward(states, net, n_lab, epoch, 0, loss, _streams_for(states, scheduler))
         ev1.record()
         ev1.synchronize()
         wall = ev0.elapsed_time(ev1) / 1e3
@@ -1143,11 +1238,13 @@ def parallel_backprop(states, net, labels, scheduler: str = "round", epoch: int 
     return states, _metrics_from_records(recs, len(states), wall, loss_v)
 
 
-def _run_step(states, net, labels, n_lab: int, epoch: int, step: int, loss_slot: torch.Tensor) -> None:
+def _run_step(states, net, labels, n_lab: int, epoch: int, step: int, loss_slot: torch.Tensor,
+              scheduler: str = "round") -> None:
     for st in states:
         st.set_labels(labels)
-    _forward(states, net, epoch, step)
-    _backward(states, net, n_lab, epoch, step, loss_slot)
+    rs = _streams_for(states, scheduler)
+    _forward(states, net, epoch, step, rs)
+    _backward(states, net, n_lab, epoch, step, loss_slot, rs)
 
 
 def train_epochs(states, net, labels, epochs: int, mode=FullBatch(), scheduler: str = "round") -> list:
@@ -1172,9 +1269,10 @@ def train_epochs(states, net, labels, epochs: int, mode=FullBatch(), scheduler: 
             for st in states:
                 st.set_labels(labels)
             evs[0].record()
+            rs = _streams_for(states, scheduler)
             for e in range(epochs):
-                _forward(states, net, e, 0)
-                _backward(states, net, n_lab, e, 0, losses[e:e + 1])
+                _forward(states, net, e, 0, rs)
+                _backward(states, net, n_lab, e, 0, losses[e:e + 1], rs)
                 evs[e + 1].record()
             evs[-1].synchronize()
             lv = (losses.cpu().numpy() / n_lab).tolist()
@@ -1182,7 +1280,7 @@ def train_epochs(states, net, labels, epochs: int, mode=FullBatch(), scheduler: 
                 wall = evs[e].elapsed_time(evs[e + 1]) / 1e3
                 out.append(_metrics_from_records(_net_records(net, epoch=e), p, wall, lv[e], states))
             return out
-        return _train_minibatch(states, net, labels, epochs, mode, dev)
+        return _train_minibatch(states, net, labels, epochs, mode, dev, scheduler)
 
 
 def _local_labelset(labels, batch: np.ndarray):
@@ -1231,7 +1329,7 @@ def _batch_operator(adjacency, batch: np.ndarray, dev):
     return normalize_adjacency(induced_pattern(adjacency, batch, add_diagonal=False), add_self_loops=True)
 
 
-def _train_minibatch(states, net, labels, epochs: int, mode, dev) -> list:
+def _train_minibatch(states, net, labels, epochs: int, mode, dev, scheduler: str = "round") -> list:
     """Mini-batch branch (runtime.py:593-632): per step a uniform sample
     (rng [seed, 0x7B]), its induced renormalised sub-adjacency, a fresh plan and
     scatter under the fixed owner array, one SGD step; weights persist."""
@@ -1255,7 +1353,7 @@ def _train_minibatch(states, net, labels, epochs: int, mode, dev) -> list:
             eff = sub_labels if sub_labels is not None else LabelSet(np.zeros(0, np.int64), np.zeros(0, np.int64),
                                                                      labels.n_classes)
             slot = torch.zeros(1, dtype=torch.float64, device=dev)
-            _run_step(sub_states, net, eff, n_lab, e, step, slot)
+            _run_step(sub_states, net, eff, n_lab, e, step, slot, scheduler)
             losses.append(float(slot.item()) / n_lab if n_lab else 0.0)
             if n_lab == 0:
                 continue  # no labelled vertex in the batch: ΔW = 0, the weights stay exactly as they were

@@ -5,8 +5,10 @@ TAG=${1:-fz}
 mkdir -p gpurun_out
 n=$(nvidia-smi -L | wc -l)
 if [ "${2:-tests}" = "tests" ]; then
-  timeout 1200 python -m pytest tests/test_gpu_distributed.py -x -q > gpurun_out/${TAG}_dist_tests.log 2>&1
+  timeout 1200 python -m pytest tests/test_gpu_distributed.py -q > gpurun_out/${TAG}_dist_tests.log 2>&1
   echo "dist tests rc=$? $(tail -1 gpurun_out/${TAG}_dist_tests.log)"
+  timeout 600 python -m pytest tests/test_gpu_path.py -q -k "threads or deterministic" > gpurun_out/${TAG}_threads.log 2>&1
+  echo "threads tests rc=$? $(tail -1 gpurun_out/${TAG}_threads.log)"
 fi
 run() {  # workload partition fuse
   local w=$1 p=$2 f=$3

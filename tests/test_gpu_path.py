@@ -186,6 +186,27 @@ class TestRuntimeSemantics:
         for a, b in zip(runs[0][1], runs[1][1]):
             assert np.array_equal(a, b)
 
+    @pytest.mark.parametrize("dims,directed", [((5, 7, 3), True), ((40, 72, 36), False)])
+    def test_threads_scheduler_matches_round(self, dims, directed):
+        """"threads" runs each rank on its own CUDA stream with event messages
+        (runtime._RankStreams); same kernels, same inputs: the round order's bits."""
+        _, a_hat, h0, labels, model, pi = self._inst(directed=directed, dims=dims)
+        out = {}
+        for sched in ("round", "threads"):
+            states = gb.scatter(a_hat, h0, pi, model, directed=directed)
+            net = gb.DeviceNetwork(4)
+            m = gb.train_epochs(states, net, labels, 2, scheduler=sched)
+            gb.parallel_feedforward(states, net, scheduler=sched, epoch=2)
+            _, mb = gb.parallel_backprop(states, net, labels, scheduler=sched, epoch=2)
+            out[sched] = ([x.loss for x in m] + [mb.loss], [np.array(w) for w in states[1].weights],
+                          [x.total_words for x in m], [np.array(st.h[-1]) for st in states])
+            if sched == "threads":
+                assert all(getattr(st, "_rank_stream", None) is not None for st in states)
+        assert out["round"][0] == out["threads"][0]
+        assert out["round"][2] == out["threads"][2]
+        for a, b in zip(out["round"][1] + out["round"][3], out["threads"][1] + out["threads"][3]):
+            assert np.array_equal(a, b)
+
     def test_message_ceiling_and_words(self):
         _, a_hat, h0, labels, model, pi = self._inst(dims=(3, 3, 3, 3), n=60)
         net = gb.DeviceNetwork(4)
