@@ -347,7 +347,11 @@ class DistributedTrainer:
         self.comm_stream = torch.cuda.Stream(device)
         # fuse the halo pack into producing kernels where one exists (FusedPack:
         # see enqueue_epoch); GCNB_FUSE_PACK=0: separate k_pack launches
-        self.fuse_pack = os.environ.get("GCNB_FUSE_PACK", "1") != "0"
+        # 0: every exchange packs with k_pack on the comm stream; 1 (default): the
+        # loss kernel packs the last layer's backward halo; 2: every producer
+        # that is one launch over all own rows packs its rows (FusedPack)
+        self.fuse_level = int(os.environ.get("GCNB_FUSE_PACK", "1"))
+        self.fuse_pack = self.fuse_level > 0
         if self.fuse_pack:
             self.st.send_map("fwd")  # device arrays built now, never inside a graph capture
             self.st.send_map("bwd")
@@ -402,7 +406,7 @@ class DistributedTrainer:
         # packed on the comm stream instead.  counter[4] serves the fused
         # producers (one at a time on the compute stream).
         def fused(phase: str, k: int):
-            if not (comm and self.fuse_pack) or k < 1 or k > L:
+            if not (comm and self.fuse_level >= 2) or k < 1 or k > L:
                 return None
             if phase == "bwd" and st.skips_bwd_exchange(k):
                 return None

@@ -14,11 +14,11 @@ run() {  # workload partition fuse
   local w=$1 p=$2 f=$3
   GCNB_FUSE_PACK=$f timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n \
     --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 400)) bench.py --gpus $n --workload $w --partition $p \
-    > gpurun_out/${TAG}_${w}_n${n}_${p}_f${f}.json 2> gpurun_out/${TAG}_${w}_n${n}_${p}_f${f}.err
-  echo "$w n=$n $p fuse=$f rc=$? $(tail -1 gpurun_out/${TAG}_${w}_n${n}_${p}_f${f}.json | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d.get("exposed_comm_pct"), d.get("e2e", {}).get("value"))' 2>&1 | tail -1)"
+    > gpurun_out/${TAG}_${w}_n${n}_${p}_f${f}_r${rep}.json 2> gpurun_out/${TAG}_${w}_n${n}_${p}_f${f}_r${rep}.err
+  echo "$w n=$n $p fuse=$f rep=$rep rc=$? $(tail -1 gpurun_out/${TAG}_${w}_n${n}_${p}_f${f}_r${rep}.json | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d.get("exposed_comm_pct"), d.get("e2e", {}).get("value"))' 2>&1 | tail -1)"
 }
-for w in amazon0601 roadnet products; do
-  run $w hp-ml 1
-  run $w hp-ml 0
+for rep in 1 2; do
+  for w in amazon0601 roadnet products; do
+    for f in 0 1 2; do run $w hp-ml $f; done
+  done
 done
-run amazon0601 hp-ml 1

@@ -38,13 +38,14 @@ def test_torchrun_parity(extra):
 @pytest.mark.parametrize("extra", [["--overlap", "off"], ["--wide", "--overlap", "on", "--graph"],
                                    ["--wide", "--directed", "--overlap", "off"]])
 def test_fused_packs_bit_identical(extra):
-    """Halo packs fused into the producers' epilogues (FusedPack) give the same
-    bits as the separate pack kernels (GCNB_FUSE_PACK=0), and they engage."""
+    """Halo packs fused into the producers' epilogues (FusedPack,
+    GCNB_FUSE_PACK=2) give the same bits as the separate pack kernels
+    (GCNB_FUSE_PACK=0), and they engage."""
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     reps = {}
-    for fuse in ("1", "0"):
+    for fuse in ("2", "0"):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                "--master-addr", "127.0.0.1", "--master-port", str(29300 + 7 * len(extra) + int(fuse)),
                str(ROOT / "scripts" / "dist_check.py"), *extra]
@@ -54,9 +55,9 @@ def test_fused_packs_bit_identical(extra):
         assert r.returncode == 0, r.stdout[-2000:] + "\n".join(errs[:20])
         reps[fuse] = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
         assert reps[fuse]["ok"], reps[fuse]
-    assert reps["1"]["weights_sha"] == reps["0"]["weights_sha"], reps
-    assert reps["1"]["losses"] == reps["0"]["losses"]
-    assert len(reps["1"]["fused_packs"]) >= 2 and not reps["0"]["fused_packs"], reps
+    assert reps["2"]["weights_sha"] == reps["0"]["weights_sha"], reps
+    assert reps["2"]["losses"] == reps["0"]["losses"]
+    assert len(reps["2"]["fused_packs"]) >= 2 and not reps["0"]["fused_packs"], reps
 
 
 def test_torchrun_minibatch_parity():
