@@ -56,6 +56,9 @@ def parse():
                          "recursive-bisection FM (C++), hp-ml = the same FM on label-propagation clusters; "
                          "gp / gp-ml = the edge-cut (graph model) twins (BASELINE config[2] compares HP/GP/RP)")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--fm-passes", dest="fm_passes", type=int, default=8,
+                    help="FM passes per bisection (the reference's default, partition.py)")
+    ap.add_argument("--restarts", type=int, default=3, help="BFS restarts per bisection (the reference's default)")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--locality", default="on", choices=("on", "off"),

@@ -13,6 +13,9 @@
 // Python (numpy Generator): the caller passes the BFS seed of every restart,
 // so small instances reproduce the reference's assignment bit-exactly.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -22,30 +25,46 @@
 
 namespace {
 
+// vertex → nets incidence, built once per bisection node and shared
+// read-only by the restarts (which run concurrently)
+struct Incidence {
+  std::vector<int64_t> vptr;
+  std::vector<int32_t> vnets;
+};
+
 struct Engine {
   int n = 0, m = 0;
   const int64_t* nptr = nullptr;   // net → pins (local vertex ids, ascending)
   const int32_t* pins = nullptr;
   const int32_t* cost = nullptr;
-  std::vector<int64_t> vptr;       // vertex → nets
-  std::vector<int32_t> vnets;
+  const int64_t* vptr = nullptr;   // vertex → nets (Incidence)
+  const int32_t* vnets = nullptr;
   std::vector<int8_t> side;
   std::vector<int32_t> c0, c1;
+  std::vector<int64_t> s0, s1;     // sum of the ids of a net's pins on side 0 / 1
   std::vector<int64_t> gain;
   int64_t cut = 0;
 
-  void init_structure(int n_, int m_, const int64_t* nptr_, const int32_t* pins_, const int32_t* cost_) {
+  static void build_incidence(int n, int m, const int64_t* nptr, const int32_t* pins, Incidence& inc) {
+    inc.vptr.assign(n + 1, 0);
+    for (int j = 0; j < m; ++j)
+      for (int64_t e = nptr[j]; e < nptr[j + 1]; ++e) ++inc.vptr[pins[e] + 1];
+    for (int v = 0; v < n; ++v) inc.vptr[v + 1] += inc.vptr[v];
+    inc.vnets.assign(inc.vptr[n], 0);
+    std::vector<int64_t> fill(inc.vptr.begin(), inc.vptr.end() - 1);
+    for (int j = 0; j < m; ++j)
+      for (int64_t e = nptr[j]; e < nptr[j + 1]; ++e) inc.vnets[fill[pins[e]]++] = j;
+  }
+
+  void init_structure(int n_, int m_, const int64_t* nptr_, const int32_t* pins_, const int32_t* cost_,
+                      const Incidence& inc) {
     n = n_; m = m_; nptr = nptr_; pins = pins_; cost = cost_;
-    vptr.assign(n + 1, 0);
-    for (int j = 0; j < m; ++j)
-      for (int64_t e = nptr[j]; e < nptr[j + 1]; ++e) ++vptr[pins[e] + 1];
-    for (int v = 0; v < n; ++v) vptr[v + 1] += vptr[v];
-    vnets.assign(vptr[n], 0);
-    std::vector<int64_t> fill(vptr.begin(), vptr.end() - 1);
-    for (int j = 0; j < m; ++j)
-      for (int64_t e = nptr[j]; e < nptr[j + 1]; ++e) vnets[fill[pins[e]]++] = j;
+    vptr = inc.vptr.data();
+    vnets = inc.vnets.data();
     c0.assign(m, 0);
     c1.assign(m, 0);
+    s0.assign(m, 0);
+    s1.assign(m, 0);
     gain.assign(n, 0);
   }
 
@@ -66,22 +85,26 @@ struct Engine {
   void rebuild() {
     std::fill(c0.begin(), c0.end(), 0);
     std::fill(c1.begin(), c1.end(), 0);
+    std::fill(s0.begin(), s0.end(), 0);
+    std::fill(s1.begin(), s1.end(), 0);
     cut = 0;
     for (int j = 0; j < m; ++j) {
-      for (int64_t e = nptr[j]; e < nptr[j + 1]; ++e) ++countr(j, side[pins[e]]);
+      for (int64_t e = nptr[j]; e < nptr[j + 1]; ++e) {
+        const int u = pins[e];
+        ++countr(j, side[u]);
+        (side[u] ? s1 : s0)[j] += u;
+      }
       if (c0[j] > 0 && c1[j] > 0) cut += cost[j];
     }
     for (int v = 0; v < n; ++v) gain[v] = gain_of(v);
   }
 
-  int single_pin_on(int j, int s, int exclude) const {
-    for (int64_t e = nptr[j]; e < nptr[j + 1]; ++e)
-      if (pins[e] != exclude && side[pins[e]] == s) return pins[e];
-    return -1;
-  }
+  // the one pin of net j on side s (count(j, s) == 1): the side's id sum, O(1)
+  int single_pin(int j, int s) const { return (int)(s ? s1[j] : s0[j]); }
 
   // move v to the other side, maintaining counts, cut and every pin's gain;
-  // on_gain(u, old, new) is called for each changed gain of u != v.
+  // on_gain(u, old, new) is called for each changed gain of u != v, after
+  // gain[u] holds the new value.
   template <class F>
   void move(int v, F&& on_gain) {
     const int sv = side[v], ov = 1 - sv;
@@ -93,24 +116,26 @@ struct Engine {
       if (t == 0) {
         for (int64_t q = nptr[j]; q < nptr[j + 1]; ++q) {
           const int u = pins[q];
-          if (u != v) { on_gain(u, gain[u], gain[u] + c); gain[u] += c; }
+          if (u != v) { gain[u] += c; on_gain(u, gain[u] - c, gain[u]); }
         }
       } else if (t == 1) {
-        const int u = single_pin_on(j, ov, v);
-        on_gain(u, gain[u], gain[u] - c);
+        const int u = single_pin(j, ov);
         gain[u] -= c;
+        on_gain(u, gain[u] + c, gain[u]);
       }
       countr(j, sv) = f - 1;
       countr(j, ov) = t + 1;
+      (sv ? s1 : s0)[j] -= v;
+      (sv ? s0 : s1)[j] += v;
       if (f - 1 == 0) {
         for (int64_t q = nptr[j]; q < nptr[j + 1]; ++q) {
           const int u = pins[q];
-          if (u != v) { on_gain(u, gain[u], gain[u] - c); gain[u] -= c; }
+          if (u != v) { gain[u] -= c; on_gain(u, gain[u] + c, gain[u]); }
         }
       } else if (f - 1 == 1) {
-        const int u = single_pin_on(j, sv, v);
-        on_gain(u, gain[u], gain[u] + c);
+        const int u = single_pin(j, sv);
         gain[u] += c;
+        on_gain(u, gain[u] - c, gain[u]);
       }
       const bool is_cut = (f - 1) > 0;
       cut += c * ((int)is_cut - (int)was_cut);
@@ -124,6 +149,7 @@ void grow_bfs(const Engine& eng, const double* w, int seed, int64_t min_count, d
               std::vector<int8_t>& side) {
   const int n = eng.n;
   std::vector<char> visited(n, 0);
+  std::vector<char> expanded(eng.m, 0);  // a net's pins are all visited once one of its pins was expanded
   std::deque<int> queue;
   queue.push_back(seed);
   visited[seed] = 1;
@@ -146,16 +172,18 @@ void grow_bfs(const Engine& eng, const double* w, int seed, int64_t min_count, d
     side[v] = 0;
     acc += wv;
     ++taken;
+    // unvisited neighbours in ascending id; a net already expanded adds none
     nb.clear();
     for (int64_t e = eng.vptr[v]; e < eng.vptr[v + 1]; ++e) {
       const int j = eng.vnets[e];
+      if (expanded[j]) continue;
+      expanded[j] = 1;
       for (int64_t q = eng.nptr[j]; q < eng.nptr[j + 1]; ++q)
-        if (eng.pins[q] != v) nb.push_back(eng.pins[q]);
+        if (!visited[eng.pins[q]]) nb.push_back(eng.pins[q]);
     }
     std::sort(nb.begin(), nb.end());
     nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
-    for (int u : nb)
-      if (!visited[u]) { visited[u] = 1; queue.push_back(u); }
+    for (int u : nb) { visited[u] = 1; queue.push_back(u); }
     if (taken >= n - min_count) break;
   }
 }
@@ -183,25 +211,68 @@ void repair_sides(std::vector<int8_t>& side, const double* w, int n, double cap,
   }
 }
 
-// Gain buckets per side with ids ordered ascending (lowest-id tie-break).
-struct Buckets {
-  int64_t off = 0;
-  std::vector<std::set<int>> b[2];
-  int64_t top[2] = {-1, -1};
+// Candidate moves of one side: the side's vertices sorted by weight at the
+// start of a pass, under a segment tree whose node holds the best unlocked
+// vertex of its range — highest gain, then LOWER id (numpy argmax's
+// tie-break).  A move of v is legal iff other + w(v) <= cap_move, i.e. iff v
+// lies in the prefix of weights <= cap_move - other, so the reference's pick
+// (the highest gain holding a legal vertex, its lowest legal id) is one prefix
+// query; a gain change or a lock re-evaluates one leaf-to-root path.
+struct MoveTree {
+  const int64_t* gain = nullptr;
+  int size = 1;
+  std::vector<int> t;         // best vertex of the node's range, -1 if none
+  std::vector<int> leaf;      // vertex -> leaf position, -1 if not on this side
+  std::vector<double> wsort;  // weights in leaf order
 
-  void reset(int64_t max_abs) {
-    off = max_abs;
-    for (int s = 0; s < 2; ++s) {
-      b[s].assign(2 * max_abs + 1, std::set<int>());
-      top[s] = -1;
+  int pick(int a, int b) const {
+    if (a < 0) return b;
+    if (b < 0) return a;
+    return (gain[a] > gain[b] || (gain[a] == gain[b] && a < b)) ? a : b;
+  }
+  void build(const std::vector<int>& verts, const double* w, int n, const int64_t* g) {
+    gain = g;
+    const int k = (int)verts.size();
+    size = 1;
+    while (size < std::max(k, 1)) size <<= 1;
+    t.assign(2 * size, -1);
+    leaf.assign(n, -1);
+    wsort.resize(k);
+    for (int i = 0; i < k; ++i) {
+      t[size + i] = verts[i];
+      leaf[verts[i]] = i;
+      wsort[i] = w[verts[i]];
     }
+    for (int x = size - 1; x >= 1; --x) t[x] = pick(t[2 * x], t[2 * x + 1]);
   }
-  void insert(int s, int64_t g, int v) {
-    const int64_t i = g + off;
-    b[s][i].insert(v);
-    if (i > top[s]) top[s] = i;
+  void refresh(int v) {
+    int x = leaf[v];
+    if (x < 0) return;
+    x = (x + size) >> 1;
+    for (; x >= 1; x >>= 1) t[x] = pick(t[2 * x], t[2 * x + 1]);
   }
-  void erase(int s, int64_t g, int v) { b[s][g + off].erase(v); }
+  void lock(int v) {
+    const int x = leaf[v];
+    if (x < 0) return;
+    t[size + x] = -1;
+    refresh(v);
+  }
+  // best vertex among the leaves [0, k)
+  int best_prefix(int k) const {
+    int res = -1;
+    int lo = size, hi = size + k;  // [lo, hi)
+    while (lo < hi) {
+      if (lo & 1) res = pick(res, t[lo++]);
+      if (hi & 1) res = pick(res, t[--hi]);
+      lo >>= 1;
+      hi >>= 1;
+    }
+    return res;
+  }
+  int best_legal(double limit) const {
+    const int k = (int)(std::upper_bound(wsort.begin(), wsort.end(), limit) - wsort.begin());
+    return k > 0 ? best_prefix(k) : -1;
+  }
 };
 
 void fm_passes(Engine& eng, const double* w, double cap, int64_t min_count, int max_passes) {
@@ -216,15 +287,9 @@ void fm_passes(Engine& eng, const double* w, double cap, int64_t min_count, int 
     total += w[v];
   }
   const double cap_move = std::max(cap, total / 2.0 + wmax);
-  int64_t max_abs = 1;
-  for (int v = 0; v < n; ++v) {
-    int64_t s = 0;
-    for (int64_t e = eng.vptr[v]; e < eng.vptr[v + 1]; ++e) s += eng.cost[eng.vnets[e]];
-    max_abs = std::max(max_abs, s);
-  }
-  Buckets bk;
+  MoveTree mt[2];
   std::vector<char> locked(n);
-  std::vector<int> moves;
+  std::vector<int> moves, verts[2];
   moves.reserve(n);
   for (int pass = 0; pass < max_passes; ++pass) {
     const int64_t start_cut = eng.cut;
@@ -232,51 +297,33 @@ void fm_passes(Engine& eng, const double* w, double cap, int64_t min_count, int 
     size_t best_len = 0;
     moves.clear();
     std::fill(locked.begin(), locked.end(), 0);
-    bk.reset(max_abs);
-    // unlocked weights per side: a side whose lightest unlocked vertex cannot
-    // move under cap_move is skipped in O(1) instead of scanning its buckets
-    std::multiset<double> wset[2];
-    for (int v = 0; v < n; ++v) {
-      bk.insert(eng.side[v], eng.gain[v], v);
-      wset[eng.side[v]].insert(w[v]);
+    for (int s = 0; s < 2; ++s) verts[s].clear();
+    for (int v = 0; v < n; ++v) verts[eng.side[v]].push_back(v);
+    for (int s = 0; s < 2; ++s) {
+      std::stable_sort(verts[s].begin(), verts[s].end(), [&](int a, int b) { return w[a] < w[b]; });
+      mt[s].build(verts[s], w, n, eng.gain.data());
     }
-    auto on_gain = [&](int u, int64_t g_old, int64_t g_new) {
-      if (locked[u]) return;
-      bk.erase(eng.side[u], g_old, u);
-      bk.insert(eng.side[u], g_new, u);
+    auto on_gain = [&](int u, int64_t, int64_t) {
+      if (!locked[u]) mt[eng.side[u]].refresh(u);
     };
     while (true) {
       int pick = -1;
       int64_t pick_gain = 0;
       for (int s = 0; s < 2; ++s) {
         if (side_n[s] - 1 < 1) continue;
-        const double other = side_w[1 - s];
-        if (wset[s].empty() || other + *wset[s].begin() > cap_move) continue;
-        for (int64_t i = bk.top[s]; i >= 0; --i) {
-          auto& set = bk.b[s][i];
-          if (set.empty()) {
-            if (i == bk.top[s]) bk.top[s] = i - 1;
-            continue;
-          }
-          int found = -1;
-          for (int v : set)
-            if (other + w[v] <= cap_move) { found = v; break; }
-          if (found >= 0) {
-            const int64_t g = i - bk.off;
-            if (pick < 0 || g > pick_gain || (g == pick_gain && found < pick)) {
-              pick = found;
-              pick_gain = g;
-            }
-            break;
-          }
+        const int found = mt[s].best_legal(cap_move - side_w[1 - s]);
+        if (found < 0) continue;
+        const int64_t g = eng.gain[found];
+        if (pick < 0 || g > pick_gain || (g == pick_gain && found < pick)) {
+          pick = found;
+          pick_gain = g;
         }
       }
       if (pick < 0) break;
       const int v = pick;
       const int s = eng.side[v];
-      bk.erase(s, eng.gain[v], v);
-      wset[s].erase(wset[s].find(w[v]));
       locked[v] = 1;
+      mt[s].lock(v);
       eng.move(v, on_gain);
       side_w[s] -= w[v];
       side_w[1 - s] += w[v];
@@ -299,6 +346,9 @@ void fm_passes(Engine& eng, const double* w, double cap, int64_t min_count, int 
       --side_n[s];
       ++side_n[1 - s];
     }
+    if (std::getenv("GCNB_HP_TRACE"))
+      std::fprintf(stderr, "  fm pass %d: %zu moves, best prefix %zu, cut %lld -> %lld\n", pass, moves.size(), best_len,
+                   (long long)start_cut, (long long)best_cut);
     if (!(best_cut < start_cut)) break;
   }
 }
@@ -317,34 +367,50 @@ int gcnb_hp_bisect(int32_t n, int32_t m, const int64_t* net_ptr, const int32_t* 
                    const double* w, double cap, int64_t min_count, const int32_t* seeds, int32_t restarts,
                    int32_t fm_passes_n, int32_t refinement, int8_t* side_out, int64_t* cut_out) {
   if (n <= 0 || m < 0 || restarts < 1 || !w || !seeds || !side_out) return 1;
-  Engine eng;
-  eng.init_structure(n, m, net_ptr, pins, cost);
+  for (int r = 0; r < restarts; ++r)
+    if (seeds[r] < 0 || seeds[r] >= n) return 1;
+  Incidence inc;
+  Engine::build_incidence(n, m, net_ptr, pins, inc);
   double total = 0.0;
   for (int v = 0; v < n; ++v) total += w[v];
-  bool have = false;
-  bool best_unbal = true;
-  int64_t best_cut = 0;
-  std::vector<int8_t> best_side;
+  // the restarts are independent (own sides, counts and gains over the shared
+  // incidence): run them concurrently, then select in restart order exactly
+  // as the sequential loop does (balanced first, then the strictly lower cut)
+  std::vector<std::vector<int8_t>> sides(restarts);
+  std::vector<int64_t> cuts(restarts, 0);
+  std::vector<char> unbals(restarts, 1);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(restarts) if (restarts > 1)
   for (int r = 0; r < restarts; ++r) {
+    Engine eng;
+    eng.init_structure(n, m, net_ptr, pins, cost, inc);
     std::vector<int8_t> side(n, 1);
-    if (seeds[r] < 0 || seeds[r] >= n) return 1;
+    auto t0 = std::chrono::steady_clock::now();
     grow_bfs(eng, w, seeds[r], min_count, total / 2.0, side);
+    auto t1 = std::chrono::steady_clock::now();
     repair_sides(side, w, n, cap, min_count);
+    auto t2 = std::chrono::steady_clock::now();
     eng.side = side;
     eng.rebuild();
+    auto t3 = std::chrono::steady_clock::now();
     if (refinement && fm_passes_n > 0) fm_passes(eng, w, cap, min_count, fm_passes_n);
+    auto t4 = std::chrono::steady_clock::now();
+    if (std::getenv("GCNB_HP_TRACE")) {
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "hp bisect n=%d r=%d bfs %.0f repair %.0f rebuild %.0f fm %.0f ms\n", n, r, ms(t0, t1),
+                   ms(t1, t2), ms(t2, t3), ms(t3, t4));
+    }
     double w0 = 0.0;
     for (int v = 0; v < n; ++v)
       if (eng.side[v] == 0) w0 += w[v];
-    const bool unbal = std::max(w0, total - w0) > cap;
-    if (!have || (unbal < best_unbal) || (unbal == best_unbal && eng.cut < best_cut)) {
-      have = true;
-      best_unbal = unbal;
-      best_cut = eng.cut;
-      best_side = eng.side;
-    }
+    unbals[r] = std::max(w0, total - w0) > cap;
+    cuts[r] = eng.cut;
+    sides[r] = std::move(eng.side);
   }
-  std::memcpy(side_out, best_side.data(), n);
+  int best = 0;
+  for (int r = 1; r < restarts; ++r)
+    if (unbals[r] < unbals[best] || (unbals[r] == unbals[best] && cuts[r] < cuts[best])) best = r;
+  const int64_t best_cut = cuts[best];
+  std::memcpy(side_out, sides[best].data(), n);
   if (cut_out) *cut_out = best_cut;
   return 0;
 }

@@ -571,23 +571,22 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
         if args.partition == "hp":
             from .hp import partition_hypergraph
 
-            # reference defaults are 8 FM passes x 3 BFS restarts; 4 x 1 keeps
-            # a 0.4 M-vertex bisection tree within ~1-2 minutes
-            pi = partition_hypergraph(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1,
+            # the reference's defaults: 8 FM passes x 3 BFS restarts (partition.py)
+            pi = partition_hypergraph(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes, restarts=args.restarts,
                                       directed=wl["directed"])
         elif args.partition == "hp-ml":
             from .hp import partition_hypergraph_ml
 
-            pi = partition_hypergraph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, labels=labels,
+            pi = partition_hypergraph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes, restarts=args.restarts, labels=labels,
                                          directed=wl["directed"])
         elif args.partition == "gp":
             from .hp import partition_graph
 
-            pi = partition_graph(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, directed=wl["directed"])
+            pi = partition_graph(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes, restarts=args.restarts, directed=wl["directed"])
         elif args.partition == "gp-ml":
             from .hp import partition_graph_ml
 
-            pi = partition_graph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=4, restarts=1, labels=labels,
+            pi = partition_graph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes, restarts=args.restarts, labels=labels,
                                     directed=wl["directed"])
         else:
             pi = random_partition(wl["a_hat"].row_nnz(), PartitionConfig(p=world, seed=args.seed, epsilon=0.01))
@@ -730,7 +729,8 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": wl["name"], "n": n, "nnz_ahat": wl["nnz"], "dims": list(wl["dims"]),
-                   "directed": wl["directed"], "partition": args.partition, "partition_s": round(t_part, 2),
+                   "directed": wl["directed"], "partition": args.partition,
+                   "fm_passes_restarts": [args.fm_passes, args.restarts], "partition_s": round(t_part, 2),
                    "locality": args.locality,
                    "l2": "flushed (512 MiB write) before every step", "graph": True, "seed": args.seed,
                    "transport": "NVLink peer stores + doorbells (CUDA IPC), P2P allreduce",

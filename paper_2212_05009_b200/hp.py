@@ -63,6 +63,8 @@ def _load():
         lib.gcnb_csr_transpose.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp]
         lib.gcnb_csr_transpose.restype = ctypes.c_int
         lib.gcnb_searchsorted_f64.argtypes = [vp, i64, vp, i64, vp]
+        lib.gcnb_coarse_column_nets.argtypes = [i64, vp, vp, vp, i64, vp, vp, vp, vp]
+        lib.gcnb_coarse_column_nets.restype = ctypes.c_int
         lib.gcnb_searchsorted_f64.restype = ctypes.c_int
         _hlib = lib
     return _hlib
@@ -139,8 +141,64 @@ def symmetrized(a):
     return CsrMatrix(n, n, rp, c, np.ones(len(c)))
 
 
+def _mix64(x: np.ndarray, salt: int) -> np.ndarray:
+    """splitmix64 finaliser of x ^ salt (uint64, wrapping)."""
+    z = x.astype(np.uint64) ^ np.uint64(salt)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def merge_identical_nets(ptr: np.ndarray, pins: np.ndarray, cost: np.ndarray):
+    """Nets with the same pin set merged into one net carrying the summed cost.
+    Every cut, every FM gain and every BFS neighbourhood of the bisection engine
+    is a sum over nets or a union of their pins, so the engine makes the same
+    moves on the merged hypergraph (tests/test_hp.py pins this); the coarse
+    hypergraphs of the multilevel partitioners repeat a pin set thousands of
+    times.  Pins of a net must be ascending (as restrict() yields them)."""
+    m = len(ptr) - 1
+    if m < 2:
+        return ptr, pins, cost
+    lens = np.diff(ptr)
+    with np.errstate(over="ignore"):
+        h1 = np.add.reduceat(_mix64(pins, 0x9E3779B97F4A7C15), ptr[:-1])
+        h2 = np.add.reduceat(_mix64(pins, 0xD1B54A32D192ED03), ptr[:-1])
+    order = np.lexsort((h2, h1, lens))
+    k1, k2, kl = h1[order], h2[order], lens[order]
+    start = np.ones(m, dtype=bool)
+    start[1:] = (k1[1:] != k1[:-1]) | (k2[1:] != k2[:-1]) | (kl[1:] != kl[:-1])
+    grp_sorted = np.cumsum(start) - 1
+    rep_of_grp = order[start]
+    rep = np.empty(m, dtype=np.int64)
+    rep[order] = rep_of_grp[grp_sorted]
+    # exact check against the representative (a hash collision keeps the net alone)
+    net_of = np.repeat(np.arange(m, dtype=np.int64), lens)
+    src = np.arange(len(pins), dtype=np.int64) - ptr[net_of] + ptr[rep[net_of]]
+    bad = np.zeros(m, dtype=bool)
+    np.logical_or.at(bad, net_of, pins != pins[src])
+    rep[bad] = np.flatnonzero(bad)
+    reps, inv = np.unique(rep, return_inverse=True)
+    if len(reps) == m:
+        return ptr, pins, cost
+    new_cost = np.bincount(inv, weights=cost.astype(np.float64), minlength=len(reps)).astype(np.int64)
+    keep = np.zeros(m, dtype=bool)
+    keep[reps] = True
+    new_ptr = np.concatenate([[0], np.cumsum(lens[reps])]).astype(np.int64)
+    new_pins = pins[keep[net_of]]
+    if new_cost.max(initial=0) > np.iinfo(np.int32).max:
+        return ptr, pins, cost
+    return new_ptr, new_pins, new_cost.astype(np.int32)
+
+
+MERGE_NETS = True  # tests switch it off to run the engine on the raw nets
+
+
 def _bisect_node(h: NetList, ids: np.ndarray, weights: np.ndarray, cap: float, min_count: int, seeds, cfg):
     ptr, pins, cost = h.restrict(ids)
+    if MERGE_NETS:
+        ptr, pins, cost = merge_identical_nets(ptr, pins, cost)
+    pins = np.ascontiguousarray(pins, dtype=np.int32)
+    cost = np.ascontiguousarray(cost, dtype=np.int32)
     w = np.ascontiguousarray(weights[ids].astype(np.float64))
     side = np.empty(len(ids), dtype=np.int8)
     seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int32))
@@ -167,11 +225,46 @@ def _recursive_bisect(h, ids, p_sub, part_base, assignment, weights, cap_leaf, r
     _recursive_bisect(h, ids[side == 1], p_sub // 2, part_base + p_sub // 2, assignment, weights, cap_leaf, rng, cfg)
 
 
-def partition_hypergraph_fm(h, cfg: PartitionConfig) -> Partition:
-    """HP on a hypergraph (NetList or gcnpart Hypergraph) — partition.py:544-559."""
+def _level_bisect(h, n, p, assignment, weights, cap_leaf, cfg, tag):
+    """The recursive bisection level by level, the nodes of a level in parallel
+    threads (the C++ engine releases the GIL and runs its restarts on OpenMP
+    threads).  Each node draws its BFS seeds from its own stream
+    default_rng([seed, tag, part_base, p_sub]), so the result does not depend
+    on the order the nodes finish in; it is not the reference's depth-first
+    draw order (partition_hypergraph_fm keeps that one for bit-exactness)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    level = [(np.arange(n, dtype=np.int64), p, 0)]
+    while level:
+        for ids, p_sub, _ in level:
+            if len(ids) < p_sub:
+                raise BalanceInfeasibleError("fewer vertices than parts in a bisection")
+
+        def one(node):
+            ids, p_sub, base = node
+            rng = np.random.default_rng([int(cfg.seed), tag, base, p_sub])
+            seeds = [int(rng.integers(0, len(ids))) for _ in range(cfg.restarts)]
+            return _bisect_node(h, ids, weights, (p_sub // 2) * cap_leaf, p_sub // 2, seeds, cfg)
+
+        with ThreadPoolExecutor(max_workers=len(level)) as ex:
+            sides = list(ex.map(one, level))
+        nxt = []
+        for (ids, p_sub, base), side in zip(level, sides):
+            for half, b in ((ids[side == 0], base), (ids[side == 1], base + p_sub // 2)):
+                if p_sub // 2 == 1:
+                    assignment[half] = b
+                else:
+                    nxt.append((half, p_sub // 2, b))
+        level = nxt
+
+
+def partition_hypergraph_fm(h, cfg: PartitionConfig, parallel: bool = False) -> Partition:
+    """HP on a hypergraph (NetList or gcnpart Hypergraph) — partition.py:544-559.
+    parallel: bisect the nodes of each recursion level concurrently (per-node
+    seed streams; used by the multilevel partitioners)."""
     if not isinstance(h, NetList):
         h = NetList.from_hypergraph(h)
-    return _partition_by_bisection(h, cfg, 0x4850)
+    return _partition_by_bisection(h, cfg, 0x4850, parallel)
 
 
 def graph_net_list(a) -> NetList:
@@ -195,7 +288,7 @@ def graph_net_list(a) -> NetList:
     return NetList(n, ptr, pins, None, np.diff(ro))
 
 
-def partition_graph_fm(g, cfg: PartitionConfig) -> Partition:
+def partition_graph_fm(g, cfg: PartitionConfig, parallel: bool = False) -> Partition:
     """GP: recursive bisection with edge-cut FM (partition.py:526-541), on a
     graph_net_list (or a gcnpart UGraph)."""
     if not isinstance(g, NetList):
@@ -205,7 +298,7 @@ def partition_graph_fm(g, cfg: PartitionConfig) -> Partition:
             raise ValueError("GP engine needs integer edge costs")
         g = NetList(g.n_vertices, np.arange(0, 2 * len(e) + 1, 2), e.reshape(-1), cost.astype(np.int64),
                     g.vertex_weight)
-    return _partition_by_bisection(g, cfg, 0x4750)
+    return _partition_by_bisection(g, cfg, 0x4750, parallel)
 
 
 def stochastic_net_list(a, batch_size: int, b: int, seed: int) -> NetList:
@@ -286,7 +379,7 @@ def partition_stochastic_ml(a_hat, batch_size: int, b: int, p: int, seed: int = 
     _, lab = np.unique(np.asarray(labels), return_inverse=True)
     h = stochastic_net_list(a_hat, batch_size, b, seed)
     cfg = PartitionConfig(p=p, epsilon=epsilon, seed=seed, fm_passes=fm_passes, restarts=restarts)
-    cpi = partition_hypergraph_fm(contract(h, lab, weights), cfg)
+    cpi = partition_hypergraph_fm(contract(h, lab, weights), cfg, parallel=True)
     owner = cpi.assignment[lab]
     pi = Partition.from_assignment(owner, weights, p, epsilon)
     if not pi.is_balanced():
@@ -294,7 +387,7 @@ def partition_stochastic_ml(a_hat, batch_size: int, b: int, p: int, seed: int = 
     return pi
 
 
-def _partition_by_bisection(h: NetList, cfg: PartitionConfig, tag: int) -> Partition:
+def _partition_by_bisection(h: NetList, cfg: PartitionConfig, tag: int, parallel: bool = False) -> Partition:
     """partition.py:503-523 over the shared C++ bisection engine."""
     n = h.n
     weights = np.asarray(h.vertex_weight, dtype=np.int64)
@@ -306,9 +399,12 @@ def _partition_by_bisection(h: NetList, cfg: PartitionConfig, tag: int) -> Parti
         raise ValueError(f"internal partitioners use recursive bisection and need p to be a power of two "
                          f"(got {cfg.p}); use an external partition file for other p")
     cap_leaf = (1.0 + cfg.epsilon) * float(weights.sum()) / cfg.p
-    rng = np.random.default_rng([int(cfg.seed), tag])
     assignment = np.full(n, -1, dtype=np.int64)
-    _recursive_bisect(h, np.arange(n, dtype=np.int64), cfg.p, 0, assignment, weights, cap_leaf, rng, cfg)
+    if parallel:
+        _level_bisect(h, n, cfg.p, assignment, weights, cap_leaf, cfg, tag)
+    else:
+        rng = np.random.default_rng([int(cfg.seed), tag])
+        _recursive_bisect(h, np.arange(n, dtype=np.int64), cfg.p, 0, assignment, weights, cap_leaf, rng, cfg)
     pi = Partition.from_assignment(assignment, weights, cfg.p, cfg.epsilon)
     if not pi.is_balanced():
         assignment = _weight_repair(assignment, weights, cfg.p, cfg.epsilon)
@@ -321,9 +417,33 @@ def _partition_by_bisection(h: NetList, cfg: PartitionConfig, tag: int) -> Parti
 def coarse_column_nets(model, labels: np.ndarray):
     """Column-net model of `model` contracted onto vertex clusters `labels`
     (0..C-1): net j's pins become the distinct clusters of its rows; nets that
-    fall inside one cluster are dropped (they can never be cut)."""
-    h = column_net_model(model)
+    fall inside one cluster are dropped (they can never be cut).  O(nnz) in
+    csrc_host/csr.cpp (gcnb_coarse_column_nets); numpy restatement below."""
     C = int(labels.max()) + 1
+    if model.n_rows != model.n_cols:
+        raise ValueError("matrix must be square")
+    w = np.bincount(labels, weights=np.asarray(model.row_nnz(), dtype=np.float64), minlength=C).astype(np.int64)
+    try:
+        lib = _load()
+    except ImportError:
+        lib = None
+    if lib is not None:
+        rp = np.ascontiguousarray(model.row_offsets, dtype=np.int64)
+        ci = np.ascontiguousarray(model.col_indices, dtype=np.int64)
+        lab = np.ascontiguousarray(labels, dtype=np.int64)
+        m, pc = ctypes.c_int64(0), ctypes.c_int64(0)
+        args = (model.n_rows, rp.ctypes.data, ci.ctypes.data, lab.ctypes.data, C, ctypes.byref(m), ctypes.byref(pc))
+        rc = lib.gcnb_coarse_column_nets(*args, None, None)
+        if rc == 0:
+            ptr = np.empty(m.value + 1, dtype=np.int64)
+            pins = np.empty(max(pc.value, 1), dtype=np.int64)
+            rc = lib.gcnb_coarse_column_nets(*args, ptr.ctypes.data, pins.ctypes.data)
+        if rc == 2:
+            raise ValueError("column-net model requires a full diagonal (self loops)")
+        if rc != 0:
+            raise ValueError("coarse column nets: invalid input")
+        return NetList(C, ptr, pins[: pc.value], None, w)
+    h = column_net_model(model)
     net_of = np.repeat(np.arange(h.n_nets, dtype=np.int64), np.diff(h.ptr))
     key = np.unique(net_of * C + labels[h.pins])
     net, cl = key // C, key % C
@@ -394,9 +514,9 @@ def _partition_ml(a_hat, p, seed, epsilon, sweeps, fm_passes, restarts, directed
         h = graph_net_list(model) if kind == "gp" else column_net_model(model)
         return (partition_graph_fm if kind == "gp" else partition_hypergraph_fm)(h, cfg)
     if kind == "gp":
-        cpi = partition_graph_fm(coarse_graph_nets(model, lab), cfg)
+        cpi = partition_graph_fm(coarse_graph_nets(model, lab), cfg, parallel=True)
     else:
-        cpi = partition_hypergraph_fm(coarse_column_nets(model, lab), cfg)
+        cpi = partition_hypergraph_fm(coarse_column_nets(model, lab), cfg, parallel=True)
     owner = cpi.assignment[lab]
     pi = Partition.from_assignment(owner, weights, p, epsilon)
     if not pi.is_balanced():

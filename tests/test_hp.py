@@ -140,3 +140,40 @@ def test_chain_keys_place_adjacent_communities_next_to_each_other():
     for t in range(1, k):                        # each is adjacent to an already-placed clique
         placed = set(order[:t].tolist())
         assert (order[t] + 1) % k in placed or (order[t] - 1) % k in placed
+
+
+def test_coarse_column_nets_native_matches_numpy(monkeypatch):
+    """gcnb_coarse_column_nets (csrc_host/csr.cpp) equals the numpy restatement."""
+    raw = o.random_undirected(400, 0.02, 11)
+    a_hat = gb.normalize_adjacency(gb.CsrMatrix(400, 400, raw.row_offsets, raw.col_indices, raw.values))
+    lab = np.random.default_rng(2).integers(0, 37, 400)
+    _, lab = np.unique(lab, return_inverse=True)
+    native = hp.coarse_column_nets(a_hat, lab)
+
+    def no_lib():
+        raise ImportError("forced")
+
+    monkeypatch.setattr(hp, "_load", no_lib)
+    ref = hp.coarse_column_nets(a_hat, lab)
+    assert np.array_equal(native.ptr, ref.ptr) and np.array_equal(native.pins, ref.pins)
+    assert np.array_equal(native.vertex_weight, ref.vertex_weight) and native.n == ref.n
+
+
+def test_merge_identical_nets_keeps_bisection(monkeypatch):
+    """Merged duplicate nets (summed costs) give the same sides as the raw nets."""
+    rng = np.random.default_rng(5)
+    n = 300
+    nets = [np.unique(rng.integers(0, n, rng.integers(2, 6))) for _ in range(900)]
+    nets = [x for x in nets if len(x) >= 2]
+    nets += nets[:400]  # duplicates
+    ptr = np.concatenate([[0], np.cumsum([len(x) for x in nets])]).astype(np.int64)
+    pins = np.concatenate(nets).astype(np.int64)
+    h = hp.NetList(n, ptr, pins, None, rng.integers(1, 5, n))
+    mp, mpins, mcost = hp.merge_identical_nets(ptr, pins.astype(np.int32), np.ones(len(nets), dtype=np.int32))
+    assert len(mp) - 1 < len(nets) and int(mcost.sum()) == len(nets)
+    cfg = gb.PartitionConfig(p=4, seed=3)
+    merged = hp.partition_hypergraph_fm(h, cfg).assignment
+    monkeypatch.setattr(hp, "MERGE_NETS", False)
+    raw_nets = hp.partition_hypergraph_fm(h, cfg).assignment
+    premerged = hp.partition_hypergraph_fm(hp.NetList(n, mp, mpins, mcost, h.vertex_weight), cfg).assignment
+    assert np.array_equal(merged, raw_nets) and np.array_equal(premerged, raw_nets)
