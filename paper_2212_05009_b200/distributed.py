@@ -538,6 +538,12 @@ class DistributedTrainer:
 # bench entry (launched by torchrun, one process per GPU)
 
 
+def _build_hash():
+    from . import build as gbuild
+
+    return gbuild.build_hash()
+
+
 def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summary, _unused, METRIC, UNIT):
     import torch
     import torch.distributed as dist
@@ -734,7 +740,7 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
                    "locality": args.locality,
                    "l2": "flushed (512 MiB write) before every step", "graph": True, "seed": args.seed,
                    "transport": "NVLink peer stores + doorbells (CUDA IPC), P2P allreduce",
-                   "overlap": tr.overlap, "reuse_fwd_aggregate": st.dw1_from_fwd},
+                   "overlap": tr.overlap, "reuse_fwd_aggregate": st.dw1_from_fwd, "build": _build_hash()},
         "e2e": {"value": round(e2e_max, 4), "unit": UNIT,
                 "h2d_bytes_per_step": int(h0_pinned.numel() * 4), "d2h_bytes_per_step": 8,
                 "input_pipeline": "epoch i+1's H2D (copy stream, pinned) overlaps epoch i; D2D staging->features"},
