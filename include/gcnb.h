@@ -208,6 +208,9 @@ int gcnb_bwd_epilogue_f32(const float* agg, int32_t ldagg, int32_t d_k, const fl
                           float* dw_partials, void* stream);
 /* (hbits, optional: sign bits of H_prev as written by gcnb_dense_bits_f32 — the
  * G_prev mask then reads ld_hbits words per row instead of H_prev's floats.) */
+/* Measurement knob: 1 = every backward layer uses the split (aggregation +
+ * dense epilogue) form when given a workspace, 0 = only large-ΔW layers. */
+int gcnb_set_split_all(int32_t on);
 /* Row stride (floats) of the optional `workspace` of gcnb_bwd_layer_f32 for
  * these widths, or 0 when the fused single-kernel form is always used.  With a
  * workspace of (own rows) × ld floats, large-ΔW layers run as an aggregation

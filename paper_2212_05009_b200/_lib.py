@@ -12,7 +12,8 @@ import ctypes
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libgcnb.so"
+# GCNB_LIB: an alternative build of the same library (A/B measurements of kernel variants)
+LIB_PATH = Path(os.environ.get("GCNB_LIB") or Path(__file__).resolve().parent / "lib" / "libgcnb.so")
 
 GCNB_OK, GCNB_EINVAL, GCNB_ECUDA, GCNB_ECOMM, GCNB_EKEY = range(5)
 ACT = {"relu": 0, "identity": 1}
@@ -68,6 +69,7 @@ _SIGNATURES = {
         [_vp, _vp, _vp, _vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp,
          _vp, _vp]),
     "gcnb_bwd_workspace_ld": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_int)]),
+    "gcnb_set_split_all": (_c_int, [_c_int]),
     "gcnb_reduce_partials_f32": (_c_int, [_vp, _c_int, _c_i64, _vp, _c_int, _vp]),
     "gcnb_reduce_sgd_f32": (_c_int, [_vp, _c_int, _c_i64, _vp, _c_int, _vp, _f32, _vp]),
     "gcnb_loss_scratch_doubles": (_c_int, []),
@@ -131,6 +133,8 @@ def load() -> ctypes.CDLL:
         check(lib.gcnb_set_watchdog_ms(int(os.environ["GCNB_WATCHDOG_MS"])))
     if os.environ.get("GCNB_DW_MODE"):
         check(lib.gcnb_set_dw_mode(int(os.environ["GCNB_DW_MODE"])))
+    if os.environ.get("GCNB_SPLIT_ALL"):  # measurement knob: aggregation + dense kernels for every layer
+        check(lib.gcnb_set_split_all(int(os.environ["GCNB_SPLIT_ALL"])))
     if os.environ.get("GCNB_AGG_GATHER"):  # tuning knob (gcnb_set_agg_gather), e.g. for A/B bench runs
         check(lib.gcnb_set_agg_gather(int(os.environ["GCNB_AGG_GATHER"])))
     return lib

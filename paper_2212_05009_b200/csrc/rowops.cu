@@ -220,6 +220,7 @@ __host__ __device__ constexpr int agg_batch(int lpr, int vpl) {
 // (sched[1] counts finished warps), so the slot is ready for the next launch
 // on the stream.
 constexpr int AGG_ROWS_PER_GRAB = 4;
+constexpr int AGG_NNZ_PER_GRAB = 1024;
 
 // FAR: the second pass of the windowed aggregation (aggwin.cu): only the far
 // entries [rp[r] + nnear[r], rp[r+1]) of the int2 entry array (`col`), added to
@@ -231,8 +232,23 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
                                             float4* __restrict__ Y4, int ldy4, int act, int* __restrict__ sched,
                                             int regs, const int* __restrict__ nnear) {
   constexpr int GPW = 32 / LPR;
-  constexpr int CH = AGG_ROWS_PER_GRAB > GPW ? AGG_ROWS_PER_GRAB / GPW : 1;  // row groups per grab
-  constexpr int RPG = GPW * CH;                                                // rows per grab
+  // Rows per ticket.  Wide rows keep AGG_ROWS_PER_GRAB (the L2 sweep window
+  // above).  Narrow rows (LPR <= 8) size the ticket to ~AGG_NNZ_PER_GRAB
+  // nonzeros from the operator's mean row length (contiguous rows: two loads
+  // of rp), up to 64 rows: with a few nonzeros per row one atomic per row
+  // group makes the shared counter the limit (roadNet fwd2, d = 8: 0.121 ->
+  // 0.068 ms; products' labelled-column bwd2: 0.56 -> 0.32 ms).
+  constexpr int CH_WIDE = AGG_ROWS_PER_GRAB > GPW ? AGG_ROWS_PER_GRAB / GPW : 1;
+  int CH = CH_WIDE;  // row groups per grab
+  if constexpr (LPR <= 8) {
+    int rows_per_grab = 16;
+    if (!rows && n_rows > 0) {
+      const int mean = max(1, (__ldg(rp + n_rows) - __ldg(rp)) / n_rows);
+      rows_per_grab = min(64, max(GPW, AGG_NNZ_PER_GRAB / mean));
+    }
+    CH = max(1, rows_per_grab / GPW);
+  }
+  const int RPG = GPW * CH;  // rows per grab
   const int lane = threadIdx.x & 31;
   const int gl = lane & (LPR - 1);
   const int gw = lane / LPR;
@@ -742,7 +758,8 @@ BwdFn pick_bwd_ipt(AggShape s, bool gp, int rpt) {
 
 // Large ΔW tiles make the fused backward kernel register-bound (2 blocks/SM):
 // then the aggregation and the dense epilogue run as two kernels.
-bool bwd_split(int d_prev, int d_k) { return (long)d_prev * round4(d_k) > 2048; }
+int g_split_all = 0;  // measurement knob (gcnb_set_split_all): split every layer
+bool bwd_split(int d_prev, int d_k) { return g_split_all || (long)d_prev * round4(d_k) > 2048; }
 
 struct BwdPlan {
   BwdFn fn;
@@ -1186,4 +1203,10 @@ extern "C" int gcnb_bwd_epilogue_pack_f32(const float* agg, int32_t ldagg, int32
   if (n_rows == 0) return GCNB_OK;
   return launch_bwd_epilogue(agg, ldagg, d_k, h_prev, ldhp, d_prev, w, g_prev, ldgp, act, nullptr, n_rows,
                              dw_partials, plan, (cudaStream_t)stream, hbits, ld_hbits, pk);
+}
+
+extern "C" int gcnb_set_split_all(int32_t on) {
+  GCNB_REQUIRE(on == 0 || on == 1, "split all: 0 or 1");
+  g_split_all = on;
+  return GCNB_OK;
 }

@@ -403,7 +403,8 @@ class ProcState:
             # aggregation + dense transform through a Y workspace
             self.fwd_ws = [None] * (L + 1)
             for k in range(1, L + 1):
-                if not self.transform_first[k] and self.dims[k - 1] * devmem.ld_of(self.dims[k]) > 2048:
+                if not self.transform_first[k] and (self.dims[k - 1] * devmem.ld_of(self.dims[k]) > 2048
+                                                    or os.environ.get("GCNB_SPLIT_ALL") == "1"):
                     self.fwd_ws[k] = torch.zeros((max(n, 1), devmem.ld_of(self.dims[k - 1])), dtype=torch.float32,
                                                  device=dev)
             self.dw1_from_fwd = bool(reuse_fwd_aggregate and L >= 1 and self.fwd_ws[1] is not None)
