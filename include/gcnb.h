@@ -211,6 +211,10 @@ int gcnb_bwd_epilogue_f32(const float* agg, int32_t ldagg, int32_t d_k, const fl
 /* Measurement knob: 1 = every backward layer uses the split (aggregation +
  * dense epilogue) form when given a workspace, 0 = only large-ΔW layers. */
 int gcnb_set_split_all(int32_t on);
+/* Engine of the fused aggregate+transform layer (gcnb_fwd_layer_f32 with W):
+ * 1 (default) = the aggregation kernel with the narrow transform in its
+ * epilogue where the widths allow it, 0 = the tile kernel.  Same sums. */
+int gcnb_set_fwd_tf(int32_t on);
 /* Row stride (floats) of the optional `workspace` of gcnb_bwd_layer_f32 for
  * these widths, or 0 when the fused single-kernel form is always used.  With a
  * workspace of (own rows) × ld floats, large-ΔW layers run as an aggregation

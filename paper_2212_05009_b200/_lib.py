@@ -70,6 +70,7 @@ _SIGNATURES = {
          _vp, _vp]),
     "gcnb_bwd_workspace_ld": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_int)]),
     "gcnb_set_split_all": (_c_int, [_c_int]),
+    "gcnb_set_fwd_tf": (_c_int, [_c_int]),
     "gcnb_reduce_partials_f32": (_c_int, [_vp, _c_int, _c_i64, _vp, _c_int, _vp]),
     "gcnb_reduce_sgd_f32": (_c_int, [_vp, _c_int, _c_i64, _vp, _c_int, _vp, _f32, _vp]),
     "gcnb_loss_scratch_doubles": (_c_int, []),
@@ -133,6 +134,8 @@ def load() -> ctypes.CDLL:
         check(lib.gcnb_set_watchdog_ms(int(os.environ["GCNB_WATCHDOG_MS"])))
     if os.environ.get("GCNB_DW_MODE"):
         check(lib.gcnb_set_dw_mode(int(os.environ["GCNB_DW_MODE"])))
+    if os.environ.get("GCNB_FWD_TF"):  # A/B knob (gcnb_set_fwd_tf)
+        check(lib.gcnb_set_fwd_tf(int(os.environ["GCNB_FWD_TF"])))
     if os.environ.get("GCNB_SPLIT_ALL"):  # measurement knob: aggregation + dense kernels for every layer
         check(lib.gcnb_set_split_all(int(os.environ["GCNB_SPLIT_ALL"])))
     if os.environ.get("GCNB_AGG_GATHER"):  # tuning knob (gcnb_set_agg_gather), e.g. for A/B bench runs

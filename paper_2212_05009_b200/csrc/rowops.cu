@@ -225,12 +225,20 @@ constexpr int AGG_NNZ_PER_GRAB = 1024;
 // FAR: the second pass of the windowed aggregation (aggwin.cu): only the far
 // entries [rp[r] + nnear[r], rp[r+1]) of the int2 entry array (`col`), added to
 // the near partial sum already in Y (order: near entries, then far entries).
-template <int LPR, int VPL, bool FAR = false>
+//
+// VPO > 0: the narrow dense transform is fused into the epilogue (the
+// aggregate-first layer with a small W, runtime.py:297-306): Y[r] =
+// act((A[r,:]·X)·W) with W (d_in × 4·c4o, zero pad columns) staged in shared
+// memory; lane gl of a row group produces output chunks gl + v·LPR (v < VPO)
+// from the group's aggregated row, broadcast chunk by chunk with shuffles.
+// The products are summed over k ascending from zero, as tile_gemm does.
+template <int LPR, int VPL, bool FAR = false, int VPO = 0>
 __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const int* __restrict__ col,
                                             const float* __restrict__ val, const int* __restrict__ rows,
                                             int n_rows, const float4* __restrict__ X4, int ldx4, int c4,
                                             float4* __restrict__ Y4, int ldy4, int act, int* __restrict__ sched,
-                                            int regs, const int* __restrict__ nnear) {
+                                            int regs, const int* __restrict__ nnear, const float4* __restrict__ W4,
+                                            int d_in, int c4o) {
   constexpr int GPW = 32 / LPR;
   // Rows per ticket.  Wide rows keep AGG_ROWS_PER_GRAB (the L2 sweep window
   // above).  Narrow rows (LPR <= 8) size the ticket to ~AGG_NNZ_PER_GRAB
@@ -244,8 +252,11 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
     int rows_per_grab = 16;
     if (!rows && n_rows > 0) {
       const int mean = max(1, (__ldg(rp + n_rows) - __ldg(rp)) / n_rows);
-      rows_per_grab = min(64, max(GPW, AGG_NNZ_PER_GRAB / mean));
+      rows_per_grab = min(64, AGG_NNZ_PER_GRAB / mean);
     }
+    // ... but not so many that half the grid's warps would get no ticket
+    // (config 1, 10 K rows: 64-row tickets left 3/4 of the warps idle)
+    rows_per_grab = min(rows_per_grab, 2 * n_rows / (int)(gridDim.x * WARPS));
     CH = max(1, rows_per_grab / GPW);
   }
   const int RPG = GPW * CH;  // rows per grab
@@ -255,6 +266,11 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
   constexpr int U = agg_batch(LPR, VPL);
   extern __shared__ __align__(16) float4 stage_all[];
   float4* stage = stage_all + (threadIdx.x >> 5) * (U * VPL * 32);
+  float4* Ws4 = stage_all + WARPS * (U * VPL * 32);  // VPO > 0: W, d_in rows of c4o chunks
+  if constexpr (VPO > 0) {
+    for (int i = threadIdx.x; i < d_in * c4o; i += NT) Ws4[i] = __ldg(W4 + i);
+    __syncthreads();
+  }
   auto grab = [&]() {
     int b = 0;
     if (lane == 0) b = atomicAdd(sched, 1);
@@ -297,7 +313,42 @@ __global__ void __launch_bounds__(NT) k_agg(const int* __restrict__ rp, const in
     if (regs == 1) aggregate_span<LPR, VPL, FAR>(col, val, s, len, X4, ldx4, c4, gl, acc);
     else if (regs == 2) aggregate_span_cp<LPR, VPL, U, true, FAR>(col, val, s, len, X4, ldx4, c4, gl, acc, stage);
     else aggregate_span_cp<LPR, VPL, U, false, FAR>(col, val, s, len, X4, ldx4, c4, gl, acc, stage);
-    if (row >= 0) {
+    if constexpr (VPO > 0) {
+      float4 o[VPO];
+#pragma unroll
+      for (int v = 0; v < VPO; ++v) o[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int ic = 0; ic < c4; ++ic) {  // warp-uniform
+        const int q = ic / LPR;
+        float4 mine = acc[0];
+#pragma unroll
+        for (int qq = 1; qq < VPL; ++qq)
+          if (qq == q) mine = acc[qq];
+        const int src = ic & (LPR - 1);
+        float a[4];
+        a[0] = __shfl_sync(0xffffffffu, mine.x, src, LPR);
+        a[1] = __shfl_sync(0xffffffffu, mine.y, src, LPR);
+        a[2] = __shfl_sync(0xffffffffu, mine.z, src, LPR);
+        a[3] = __shfl_sync(0xffffffffu, mine.w, src, LPR);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int k = 4 * ic + e;
+          if (k < d_in) {
+#pragma unroll
+            for (int v = 0; v < VPO; ++v) {
+              const int oc = gl + v * LPR;
+              if (oc < c4o) o[v] = fma4(a[e], Ws4[k * c4o + oc], o[v]);
+            }
+          }
+        }
+      }
+      if (row >= 0) {
+#pragma unroll
+        for (int v = 0; v < VPO; ++v) {
+          const int oc = gl + v * LPR;
+          if (oc < c4o) Y4[(size_t)row * ldy4 + oc] = act_fwd4(o[v], act);
+        }
+      }
+    } else if (row >= 0) {
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
         const int ch = gl + q * LPR;
@@ -704,7 +755,7 @@ int tile_rows(int d_out, int lpr, int* rpt_out) {
 #define GCNB_LPR_CASES(M) M(2, 1) M(4, 1) M(8, 1) M(16, 1) M(32, 1) M(32, 2)
 
 using AggFn = void (*)(const int*, const int*, const float*, const int*, int, const float4*, int, int, float4*, int,
-                       int, int*, int, const int*);
+                       int, int*, int, const int*, const float4*, int, int);
 // Shape of the aggregation-only kernel over all own rows: two float4 chunks per
 // lane from 9 chunks up, so 2-4 rows share a warp (rows of similar length side by
 // side after the degree-sorted layout windows): measured on the products shape,
@@ -759,6 +810,7 @@ BwdFn pick_bwd_ipt(AggShape s, bool gp, int rpt) {
 // Large ΔW tiles make the fused backward kernel register-bound (2 blocks/SM):
 // then the aggregation and the dense epilogue run as two kernels.
 int g_split_all = 0;  // measurement knob (gcnb_set_split_all): split every layer
+int g_fwd_tf = 1;     // gcnb_set_fwd_tf: 1 = k_agg with the fused transform, 0 = tile kernel k_fwd_gemm
 bool bwd_split(int d_prev, int d_k) { return g_split_all || (long)d_prev * round4(d_k) > 2048; }
 
 struct BwdPlan {
@@ -844,7 +896,66 @@ int launch_agg(const int32_t* row_ptr, const int32_t* col, const float* val, con
   int* sched = sched_counter(st);
   GCNB_REQUIRE(sched != nullptr, "%s: no work-counter slot for this stream", what);
   fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, reinterpret_cast<const float4*>(x), ldx / 4,
-                             round4(d) / 4, reinterpret_cast<float4*>(y), ldy / 4, act, sched, g_agg_regs, nnear);
+                             round4(d) / 4, reinterpret_cast<float4*>(y), ldy / 4, act, sched, g_agg_regs, nnear,
+                             nullptr, 0, 0);
+  GCNB_AFTER_LAUNCH(what);
+  return GCNB_OK;
+}
+
+// Aggregate-first layer with the narrow transform fused into k_agg's epilogue
+// (VPO output chunks per lane): rows handed out dynamically like the plain
+// aggregation, W in shared memory.  agg_tf_shape says whether the widths have
+// such a kernel (otherwise the tile kernel k_fwd_gemm runs the layer).
+AggFn pick_agg_tf(int lpr, int vpo) {
+#define M(L)                                                    \
+  if (lpr == L) {                                               \
+    if (vpo == 1) return k_agg<L, 1, false, 1>;                 \
+    if (vpo == 2) return k_agg<L, 1, false, 2>;                 \
+    if (vpo == 4) return k_agg<L, 1, false, 4>;                 \
+  }
+  M(2) M(4) M(8) M(16)
+#undef M
+  return nullptr;
+}
+
+bool agg_tf_shape(int d_in, int d_out, int* lpr, int* vpo) {
+  const AggShape s = agg_shape(d_in);
+  if (s.vpl != 1 || s.lpr > 16) return false;
+  const int c4o = round4(d_out) / 4;
+  const int v = (c4o + s.lpr - 1) / s.lpr;
+  const int vp = v <= 1 ? 1 : v <= 2 ? 2 : v <= 4 ? 4 : 0;
+  if (!vp) return false;
+  *lpr = s.lpr;
+  *vpo = vp;
+  return true;
+}
+
+int launch_agg_tf(const int32_t* row_ptr, const int32_t* col, const float* val, const int32_t* rows, int32_t n_rows,
+                  const float* x, int32_t ldx, int32_t d_in, const float* w, int32_t d_out, float* y, int32_t ldy,
+                  int32_t act, cudaStream_t st, const char* what) {
+  int lpr = 0, vpo = 0;
+  GCNB_REQUIRE(agg_tf_shape(d_in, d_out, &lpr, &vpo), "%s: no fused narrow transform for %d -> %d", what, d_in,
+               d_out);
+  AggFn fn = pick_agg_tf(lpr, vpo);
+  GCNB_REQUIRE(fn != nullptr, "%s: no kernel for lpr=%d vpo=%d", what, lpr, vpo);
+  const int c4o = round4(d_out) / 4;
+  const size_t smem = (size_t)WARPS * agg_batch(lpr, 1) * 32 * sizeof(float4) + (size_t)d_in * c4o * sizeof(float4);
+  GCNB_REQUIRE(smem <= 200 * 1024, "%s: W tile too large for the fused transform", what);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn), NT, smem) !=
+          cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  const int rows_per_block = NT / lpr;
+  const int grid = std::max(1, std::min((n_rows + rows_per_block - 1) / rows_per_block, num_sms() * per_sm));
+  int* sched = sched_counter(st);
+  GCNB_REQUIRE(sched != nullptr, "%s: no work-counter slot for this stream", what);
+  fn<<<grid, NT, smem, st>>>(row_ptr, col, val, rows, n_rows, reinterpret_cast<const float4*>(x), ldx / 4,
+                             round4(d_in) / 4, reinterpret_cast<float4*>(y), ldy / 4, act, sched, g_agg_regs,
+                             nullptr, reinterpret_cast<const float4*>(w), d_in, c4o);
   GCNB_AFTER_LAUNCH(what);
   return GCNB_OK;
 }
@@ -922,6 +1033,10 @@ extern "C" int gcnb_fwd_layer_f32(const int32_t* row_ptr, const int32_t* col, co
   cudaStream_t st = (cudaStream_t)stream;
   if (!w)  // aggregate-only: no tile (no barrier, full occupancy)
     return launch_agg(row_ptr, col, val, rows, n_rows, x, ldx, d_in, h, ldh, act, st, "fwd layer (aggregate)");
+  int lpr = 0, vpo = 0;
+  if (g_fwd_tf && agg_tf_shape(d_in, d_out, &lpr, &vpo))
+    return launch_agg_tf(row_ptr, col, val, rows, n_rows, x, ldx, d_in, w, d_out, h, ldh, act, st,
+                         "fwd layer (aggregate+transform, fused epilogue)");
   return launch_fwd_gemm(true, row_ptr, col, val, rows, n_rows, x, ldx, d_in, w, d_out, h, ldh, act, st,
                          "fwd layer (aggregate+transform)");
 }
@@ -1208,5 +1323,11 @@ extern "C" int gcnb_bwd_epilogue_pack_f32(const float* agg, int32_t ldagg, int32
 extern "C" int gcnb_set_split_all(int32_t on) {
   GCNB_REQUIRE(on == 0 || on == 1, "split all: 0 or 1");
   g_split_all = on;
+  return GCNB_OK;
+}
+
+extern "C" int gcnb_set_fwd_tf(int32_t on) {
+  GCNB_REQUIRE(on == 0 || on == 1, "fwd tf: 0 or 1");
+  g_fwd_tf = on;
   return GCNB_OK;
 }

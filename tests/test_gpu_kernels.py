@@ -123,6 +123,29 @@ def test_fwd_layer_fused_transform(d_in, d_out, act):
     assert np.all(pad == 0), "pad columns must stay zero"
 
 
+@pytest.mark.parametrize("d_in,d_out", [(16, 16), (12, 16), (8, 16), (8, 32), (3, 4), (5, 7), (20, 40), (32, 48),
+                                        (2, 60)])
+@pytest.mark.parametrize("with_rows", [False, True])
+def test_fwd_layer_fused_epilogue_matches_tile_kernel(d_in, d_out, with_rows):
+    """k_agg with the narrow transform in its epilogue (gcnb_set_fwd_tf 1, the
+    default) gives the tile kernel's bits (gcnb_set_fwd_tf 0): same CSR-order
+    aggregation, same k-ascending products; row lists and empty rows too."""
+    a = rand_csr(2100, 2100, 0.004, d_in * 31 + d_out, empty_rows=25)
+    x = np.random.default_rng(11).standard_normal((2100, d_in))
+    w = np.random.default_rng(12).uniform(-0.4, 0.4, (d_in, d_out))
+    rows = np.sort(np.random.default_rng(13).choice(2100, 777, replace=False)) if with_rows else None
+    try:
+        _lib.call("gcnb_set_fwd_tf", 1)
+        got_tf, _ = _fwd(a, x, w, "relu", rows)
+        _lib.call("gcnb_set_fwd_tf", 0)
+        got_tile, _ = _fwd(a, x, w, "relu", rows)
+    finally:
+        _lib.call("gcnb_set_fwd_tf", 1)
+    sel = rows if rows is not None else slice(None)
+    assert np.array_equal(got_tf[sel], got_tile[sel])
+    close(got_tf[sel], o.act_and_grad("relu", o.dmm(o.spmm(a, x), w))[0][sel])
+
+
 def test_fwd_layer_aggregate_only_relu_and_rows():
     a = rand_csr(1200, 1200, 0.01, 3)
     x = np.random.default_rng(7).standard_normal((1200, 48))
