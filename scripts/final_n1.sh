@@ -1,0 +1,14 @@
+#!/bin/bash
+# Round-end evidence on one B200: the GPU test suite, smoke(), the default bench line, the reference arm,
+# and the ncu launch list + full capture of the default workload (each ncu command only after the same
+# command exited 0 without ncu).  usage (under gpurun): bash scripts/final_n1.sh tag
+TAG=${1:-fin}
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/${TAG}_pytest.log)"
+timeout 600 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$? $(tail -1 gpurun_out/${TAG}_smoke.log)"
+timeout 1200 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$? $(tail -1 gpurun_out/${TAG}_bench.json | cut -c1-150)"
+timeout 1200 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err; echo "ref rc=$? $(tail -1 gpurun_out/${TAG}_ref.json | cut -c1-150)"
+CMD="python bench.py --steps 3 --warmup 3 --kernels-only --no-products3"
+$CMD > gpurun_out/${TAG}_plain.json 2>&1; echo "plain rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_agg|k_dense_tc|k_dw_tc|k_loss" -c 8 -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
