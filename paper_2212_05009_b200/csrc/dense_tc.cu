@@ -26,6 +26,10 @@
 
 namespace gcnb {
 
+// Extra dynamic shared memory each tcgen05 kernel asks for so that it can align
+// its stage ring to 1024 bytes itself (swizzle atoms).
+constexpr size_t SMEM_ALIGN_PAD = 1024;
+
 namespace {
 
 
@@ -179,7 +183,10 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
                const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmm,
                const EpiPack pk) {
   constexpr bool MASKED = MK != 0;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // swizzle atoms need 1024-byte alignment: align by hand (the launch adds
+  // SMEM_ALIGN_PAD bytes) rather than trust the placement of the dynamic region
+  uint8_t* const smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bars[4 * DT_MAX_STAGES + 4];
   __shared__ uint32_t tmem_base_slot;
   const int Kp = (K + 7) & ~7, kc = (K + 3) / 4;  // MMA K extent, loaded chunks per row
@@ -194,7 +201,6 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
   // barriers: full[S] hi_done[S] lo_ready[S] empty[S] | acc_full[2] acc_empty[2]
   auto bar = [&](int kind, int i) { return smem_u32(&bars[kind * DT_MAX_STAGES + i]); };
   auto abar = [&](int kind, int i) { return smem_u32(&bars[4 * DT_MAX_STAGES + 2 * kind + i]); };
-  if (smem_u32(smem) & 1023u) __trap();           // swizzle atoms need 1024-byte alignment
 
   // K pad chunks of every X stage are never loaded: zero them once
   const int pad_ch = Kp / 4 - kc;
@@ -437,7 +443,7 @@ __global__ void __launch_bounds__(DT_THREADS, 1)
 }
 
 namespace {
-constexpr size_t DT_SMEM_MAX = 227 * 1024 - 1024;
+constexpr size_t DT_SMEM_MAX = 227 * 1024 - 1024;  // leaves room for SMEM_ALIGN_PAD
 
 // Rows per tile (MMA N) and stage count: the largest tile of 128/64/32 rows
 // for which enough stages fit (up to DT_MAX_STAGES).  The cp.async producer
@@ -548,6 +554,7 @@ int launch_dense_tc(const float* x, int ldx, const int* rows, int n_rows, int d_
                      : (relu ? k_dense_tc<true, 0, T> : k_dense_tc<false, 0, T>))
   Fn fn = tma ? GCNB_DT_PICK(true) : GCNB_DT_PICK(false);
 #undef GCNB_DT_PICK
+  smem += SMEM_ALIGN_PAD;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles = (n_rows + nt - 1) / nt;
   const int grid = std::max(1, std::min(tiles, num_sms()));
@@ -644,7 +651,10 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
     k_dw_tc(const float* __restrict__ H, int ldh, int d_prev, const float* __restrict__ A, int lda, int d_k,
             const int* __restrict__ rows, int n_rows, float* __restrict__ partials, int n_slots,
             const __grid_constant__ CUtensorMap tmh, const __grid_constant__ CUtensorMap tma_) {
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // swizzle atoms need 1024-byte alignment: align by hand (the launch adds
+  // SMEM_ALIGN_PAD bytes) rather than trust the placement of the dynamic region
+  uint8_t* const smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bars[3 * DW_MAX_STAGES + 1];
   __shared__ uint64_t accb[4];  // accumulator full[2] (MMA commit) / empty[2] (128 epilogue arrivals)
   __shared__ uint32_t tmem_base_slot;
@@ -666,7 +676,6 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
   // barriers: full[S] (producers) conv[S] (converters) empty[S] (MMA commit) | done
   auto bar = [&](int kind, int i) { return smem_u32(&bars[kind * DW_MAX_STAGES + i]); };
   const uint32_t b_done = smem_u32(&bars[3 * DW_MAX_STAGES]);
-  if (smem_u32(smem) & 1023u) __trap();
 
   // pad features (never loaded) must read as zero in every buffer: clear once
   for (int i = threadIdx.x; i < S * g.st_bytes / 16; i += DW_THREADS)
@@ -888,7 +897,10 @@ __host__ __device__ inline Dw2Geom dw2_geom(int d_prev, int d_k) {
 __global__ void __launch_bounds__(DW2_THREADS, 1)
     k_dw_tc2(int d_prev, int d_k, int n_rows, float* __restrict__ partials, int n_slots,
              const __grid_constant__ CUtensorMap tmh, const __grid_constant__ CUtensorMap tma_) {
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // swizzle atoms need 1024-byte alignment: align by hand (the launch adds
+  // SMEM_ALIGN_PAD bytes) rather than trust the placement of the dynamic region
+  uint8_t* const smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bars[3 * DW2_MAX_STAGES + 1];
   __shared__ uint64_t accb[4];
   __shared__ uint32_t tmem_base_slot;
@@ -903,7 +915,6 @@ __global__ void __launch_bounds__(DW2_THREADS, 1)
   auto st_al = [&](int s) { return smem + s * g.st_bytes + g.h_bytes + g.a_bytes; };
   auto bar = [&](int kind, int i) { return smem_u32(&bars[kind * DW2_MAX_STAGES + i]); };
   const uint32_t b_done = smem_u32(&bars[3 * DW2_MAX_STAGES]);
-  if (smem_u32(smem) & 1023u) __trap();
   // lo(A) pad columns (never loaded) must read as zero: clear once
   for (int i = threadIdx.x; i < S * g.st_bytes / 16; i += DW2_THREADS)
     reinterpret_cast<float4*>(smem)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1099,7 +1110,7 @@ int launch_dw_tc(const float* h, int ldh, int d_prev, const float* a, int lda, i
     CUtensorMap tmh2;
     std::memset(&tmh2, 0, sizeof(tmh2));
     if (tmap_2d(&tmh2, h, d_prev, n_rows, ldh, g2.hstride, DW_T, CU_TENSOR_MAP_SWIZZLE_NONE)) {
-      const size_t smem2 = (size_t)g2.stages * g2.st_bytes;
+      const size_t smem2 = (size_t)g2.stages * g2.st_bytes + SMEM_ALIGN_PAD;
       cudaFuncSetAttribute(k_dw_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
       k_dw_tc2<<<grid, DW2_THREADS, smem2, st>>>(d_prev, d_k, n_rows, partials, n_slots, tmh2, tma_);
       GCNB_AFTER_LAUNCH("bwd ΔW (tcgen05 3xTF32, Hᵀ in TMEM, TMA)");
@@ -1107,8 +1118,9 @@ int launch_dw_tc(const float* h, int ldh, int d_prev, const float* a, int lda, i
     }
   }
   auto fn = tma ? k_dw_tc<true> : k_dw_tc<false>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fn<<<grid, DW_THREADS, smem, st>>>(h, ldh, d_prev, a, lda, d_k, rows, n_rows, partials, n_slots, tmh, tma_);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + SMEM_ALIGN_PAD));
+  fn<<<grid, DW_THREADS, smem + SMEM_ALIGN_PAD, st>>>(h, ldh, d_prev, a, lda, d_k, rows, n_rows, partials, n_slots,
+                                                      tmh, tma_);
   GCNB_AFTER_LAUNCH(tma ? "bwd ΔW (tcgen05 3xTF32, TMA)" : "bwd ΔW (tcgen05 3xTF32)");
   return GCNB_OK;
 }
