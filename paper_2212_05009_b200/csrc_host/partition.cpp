@@ -416,3 +416,86 @@ int gcnb_hp_bisect(int32_t n, int32_t m, const int64_t* net_ptr, const int32_t* 
 }
 
 }  // extern "C"
+
+// k-way boundary refinement of a p-way partition under the connectivity-1 cost
+// of the column-net model of a SYMMETRIC pattern (net j pins the rows of
+// column j, i.e. of row j): the uncoarsening step of the multilevel
+// partitioners (hp.py), after a projected coarse partition.  Vertices are
+// visited in id order; each moves to the part with the largest positive gain
+//   gain(v, a -> b) = #{nets j of v : cnt[j][a] == 1} - #{nets j of v : cnt[j][b] == 0}
+// (lowest part id on ties) if that part stays within `cap` and `a` keeps a
+// vertex.  Only strictly improving moves: the cost never increases, and the
+// result is deterministic.  owner (int64) is updated in place; *moved_out /
+// *gain_out report the moves and the total cost reduction.
+extern "C" int gcnb_kway_refine(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* owner, int32_t p,
+                                const int64_t* weight, double cap, int32_t passes, int64_t* moved_out,
+                                int64_t* gain_out) {
+  if (n < 0 || p < 2 || p > 1024 || !rp || !ci || !owner || !weight) return 1;
+  std::vector<int32_t> cnt((size_t)n * p, 0);
+  std::vector<double> load(p, 0.0);
+  std::vector<int64_t> members(p, 0);
+  for (int64_t v = 0; v < n; ++v) {
+    const int64_t a = owner[v];
+    if (a < 0 || a >= p) return 1;
+    load[a] += (double)weight[v];
+    ++members[a];
+  }
+  for (int64_t j = 0; j < n; ++j)  // net j's pins: row j of the symmetric pattern
+    for (int64_t e = rp[j]; e < rp[j + 1]; ++e) {
+      const int64_t u = ci[e];
+      if (u < 0 || u >= n) return 1;
+      ++cnt[(size_t)j * p + owner[u]];
+    }
+  std::vector<int64_t> gain(p);
+  std::vector<char> seen(p);
+  int64_t moved = 0, total = 0;
+  for (int pass = 0; pass < passes; ++pass) {
+    int64_t moved_pass = 0;
+    for (int64_t v = 0; v < n; ++v) {
+      const int64_t a = owner[v];
+      if (members[a] <= 1) continue;
+      // candidate parts: those some net of v already touches
+      std::fill(gain.begin(), gain.end(), 0);
+      std::fill(seen.begin(), seen.end(), 0);
+      int64_t leave = 0;  // nets where v is the only pin in a
+      for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+        const int32_t* c = &cnt[(size_t)ci[e] * p];
+        if (c[a] == 1) ++leave;
+        for (int q = 0; q < p; ++q)
+          if (c[q] > 0) seen[q] = 1;
+      }
+      if (!leave) continue;  // no net would lose part a: no move can gain
+      int best = -1;
+      int64_t best_gain = 0;
+      for (int q = 0; q < p; ++q) {
+        if (q == a || !seen[q] || load[q] + (double)weight[v] > cap) continue;
+        int64_t join = 0;  // nets of v with no pin in q yet
+        for (int64_t e = rp[v]; e < rp[v + 1]; ++e)
+          if (cnt[(size_t)ci[e] * p + q] == 0) ++join;
+        const int64_t g = leave - join;
+        if (g > best_gain) {
+          best_gain = g;
+          best = q;
+        }
+      }
+      if (best < 0) continue;
+      for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+        int32_t* c = &cnt[(size_t)ci[e] * p];
+        --c[a];
+        ++c[best];
+      }
+      load[a] -= (double)weight[v];
+      load[best] += (double)weight[v];
+      --members[a];
+      ++members[best];
+      owner[v] = best;
+      total += best_gain;
+      ++moved_pass;
+    }
+    moved += moved_pass;
+    if (!moved_pass) break;
+  }
+  if (moved_out) *moved_out = moved;
+  if (gain_out) *gain_out = total;
+  return 0;
+}

@@ -64,6 +64,8 @@ def _load():
         lib.gcnb_csr_transpose.restype = ctypes.c_int
         lib.gcnb_searchsorted_f64.argtypes = [vp, i64, vp, i64, vp]
         lib.gcnb_coarse_column_nets.argtypes = [i64, vp, vp, vp, i64, vp, vp, vp, vp]
+        lib.gcnb_kway_refine.argtypes = [i64, vp, vp, vp, ctypes.c_int32, vp, f64, ctypes.c_int32, vp, vp]
+        lib.gcnb_kway_refine.restype = ctypes.c_int
         lib.gcnb_coarse_column_nets.restype = ctypes.c_int
         lib.gcnb_searchsorted_f64.restype = ctypes.c_int
         _hlib = lib
@@ -493,7 +495,26 @@ def partition_hypergraph_ml(a_hat, p: int, seed: int = 0, epsilon: float = 0.01,
     return _partition_ml(a_hat, p, seed, epsilon, sweeps, fm_passes, restarts, directed, labels, "hp")
 
 
-def _partition_ml(a_hat, p, seed, epsilon, sweeps, fm_passes, restarts, directed, labels, kind) -> Partition:
+def kway_refine(model, owner: np.ndarray, p: int, weights, epsilon: float, passes: int = 4):
+    """Greedy k-way boundary refinement (csrc_host/partition.cpp gcnb_kway_refine)
+    of `owner` under the connectivity-1 cost of the column-net model of the
+    symmetric pattern `model`, within the balance cap: the uncoarsening step of
+    the multilevel partitioners.  Returns (refined owner, moves, cost reduction)."""
+    rp = np.ascontiguousarray(model.row_offsets, dtype=np.int64)
+    ci = np.ascontiguousarray(model.col_indices, dtype=np.int64)
+    w = np.ascontiguousarray(weights, dtype=np.int64)
+    out = np.ascontiguousarray(owner, dtype=np.int64).copy()
+    cap = (1.0 + epsilon) * float(w.sum()) / p
+    moved, gain = ctypes.c_int64(0), ctypes.c_int64(0)
+    rc = _load().gcnb_kway_refine(model.n_rows, rp.ctypes.data, ci.ctypes.data, out.ctypes.data, p, w.ctypes.data,
+                                  cap, passes, ctypes.byref(moved), ctypes.byref(gain))
+    if rc != 0:
+        raise ValueError("kway refine: invalid input")
+    return out, int(moved.value), int(gain.value)
+
+
+def _partition_ml(a_hat, p, seed, epsilon, sweeps, fm_passes, restarts, directed, labels, kind,
+                  refine: bool = True) -> Partition:
     from .locality import community_labels
 
     if directed is None:
@@ -521,6 +542,10 @@ def _partition_ml(a_hat, p, seed, epsilon, sweeps, fm_passes, restarts, directed
     pi = Partition.from_assignment(owner, weights, p, epsilon)
     if not pi.is_balanced():
         pi = Partition.from_assignment(_weight_repair(owner, weights, p, epsilon), weights, p, epsilon)
+    if kind == "hp" and refine:
+        # uncoarsening: vertex-level moves the cluster-level FM could not make
+        owner, _, _ = kway_refine(model, pi.assignment, p, weights, epsilon)
+        pi = Partition.from_assignment(owner, weights, p, epsilon)
     return pi
 
 

@@ -177,3 +177,20 @@ def test_merge_identical_nets_keeps_bisection(monkeypatch):
     raw_nets = hp.partition_hypergraph_fm(h, cfg).assignment
     premerged = hp.partition_hypergraph_fm(hp.NetList(n, mp, mpins, mcost, h.vertex_weight), cfg).assignment
     assert np.array_equal(merged, raw_nets) and np.array_equal(premerged, raw_nets)
+
+
+def test_kway_refine_never_increases_cost_and_keeps_balance():
+    """gcnb_kway_refine: strictly improving vertex moves under the balance cap."""
+    raw = o.random_undirected(900, 0.01, 4)
+    a_hat = gb.normalize_adjacency(gb.CsrMatrix(900, 900, raw.row_offsets, raw.col_indices, raw.values))
+    w = np.asarray(a_hat.row_nnz(), dtype=np.int64)
+    start = np.random.default_rng(3).integers(0, 4, 900)
+    pi0 = gb.Partition.from_assignment(start, w, 4, 0.5)
+    owner, moved, gain = hp.kway_refine(a_hat, pi0.assignment, 4, w, 0.5)
+    v0 = gb.plan_volume(gb.build_comm_plan(a_hat, pi0), 1).total_words
+    pi1 = gb.Partition.from_assignment(owner, w, 4, 0.5)
+    v1 = gb.plan_volume(gb.build_comm_plan(a_hat, pi1), 1).total_words
+    assert moved > 0 and gain > 0 and v1 == v0 - gain  # the gain is exactly the connectivity-1 reduction
+    assert pi1.is_balanced()
+    again, _, _ = hp.kway_refine(a_hat, pi0.assignment, 4, w, 0.5)
+    assert np.array_equal(owner, again)
