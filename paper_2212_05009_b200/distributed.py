@@ -835,7 +835,8 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
 
             prof.disable()
             buf = io.StringIO()
-            pstats.Stats(prof, stream=buf).sort_stats("cumulative").print_stats(30)
+            pstats.Stats(prof, stream=buf).sort_stats("cumulative").print_stats(45)
+            pstats.Stats(prof, stream=buf).sort_stats("tottime").print_stats(25)
             print(buf.getvalue(), file=sys.stderr, flush=True)
         t3 = time.perf_counter()
         tr.enqueue_epoch(0)
