@@ -22,13 +22,31 @@ from .comm import CommPlan, _owner_and_p
 from .layout import OpLayout, RankLayout, degree_windows
 
 _COL_MASK = (1 << 49) - 1
+_TIMING = False  # scripts/setup_timing.py: per-stage device-synced timings
+
+
+def _tick(label, t0):
+    if not _TIMING:
+        return t0
+    import time
+
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    print(f"    {label:26s} {1e3 * (t1 - t0):8.1f} ms", flush=True)
+    return t1
 
 
 class _DevCsr:
     """fp64 CSR of the (square) operator on the device, int64 indices."""
 
     def __init__(self, a, dev):
+        from .devingest import DeviceGraph
+
         self.n = int(a.n_rows)
+        if isinstance(a, DeviceGraph):  # already resident (mini-batch operators): no copies
+            self.rp, self.ci, self.val = a.rp, a.ci, a.val
+            self.rp_host = a.rp.cpu().numpy()
+            return
         self.rp_host = np.asarray(a.row_offsets, dtype=np.int64)
         self.rp = torch.from_numpy(np.array(self.rp_host)).to(dev)
         self.ci = torch.from_numpy(np.array(a.col_indices, dtype=np.int64)).to(dev)
@@ -37,6 +55,9 @@ class _DevCsr:
 
 def _plan(dcsr: _DevCsr, owner: np.ndarray, p: int, dev):
     """(CommPlan, device keys, pair bounds (host), rows_sorted, rank_ptr (host), localpos)."""
+    import time
+
+    tt = _tick("plan: start", time.perf_counter())
     n = dcsr.n
     own_d = torch.from_numpy(owner.astype(np.int32)).to(dev)
     bounds = torch.zeros(p * p + 1, dtype=torch.int64, device=dev)
@@ -48,11 +69,13 @@ def _plan(dcsr: _DevCsr, owner: np.ndarray, p: int, dev):
     _lib.call("gcnb_plan_build", dcsr.rp.data_ptr(), dcsr.ci.data_ptr(), n, own_d.data_ptr(), p, ctypes.byref(kp),
               ctypes.byref(nk), bounds.data_ptr(), rows_sorted.data_ptr(), rank_ptr.data_ptr(), localpos.data_ptr(),
               torch.cuda.current_stream(dev).cuda_stream)
+    tt = _tick("plan: gcnb_plan_build", tt)
     n_keys = int(nk.value)
     keys_host = np.empty(n_keys, dtype=np.uint64)
     if n_keys:
         _lib.call("gcnb_copy_d2h", keys_host.ctypes.data, kp.value, 8 * n_keys)
     b = bounds.cpu().numpy()
+    tt = _tick(f"plan: keys D2H ({n_keys})", tt)
     cols = (keys_host & np.uint64(_COL_MASK)).astype(np.int64)
     empty = np.zeros(0, dtype=np.int64)
     # keys are sorted by (consumer, sender, column): block (c, s) = send[s][c]
@@ -60,6 +83,7 @@ def _plan(dcsr: _DevCsr, owner: np.ndarray, p: int, dev):
                        else empty.copy() for c in range(p)) for s in range(p))
     recv_from = tuple(np.array([s for s in range(p) if len(send[s][m])], dtype=np.int64) for m in range(p))
     plan = CommPlan(p, owner.astype(np.int64), send, recv_from)
+    _tick("plan: host send lists", tt)
     return plan, kp.value, b, rows_sorted, rank_ptr.cpu().numpy(), localpos
 
 
@@ -81,6 +105,9 @@ def build_plan_device(a, pi, p: int | None = None, device=None) -> CommPlan:
 
 def _op_layout(dcsr: _DevCsr, plan: CommPlan, kptr: int, bounds: np.ndarray, m: int, rows: np.ndarray, dev,
                sort_rows: bool = True) -> OpLayout:
+    import time
+
+    tt = _tick("layout: start", time.perf_counter())
     p = plan.p
     n = dcsr.n
     n_own = len(rows)
@@ -104,6 +131,7 @@ def _op_layout(dcsr: _DevCsr, plan: CommPlan, kptr: int, bounds: np.ndarray, m: 
     _lib.call("gcnb_layout_fill", dcsr.rp.data_ptr(), dcsr.ci.data_ptr(), dcsr.val.data_ptr(), n, rows_d.data_ptr(),
               n_own, kptr, k0, n_halo, int(bool(sort_rows)), row_ptr.data_ptr(), ext.data_ptr(), val.data_ptr(),
               has_halo.data_ptr(), colmap.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+    tt = _tick("layout: gcnb_layout_fill", tt)
     hh = has_halo.cpu().numpy()[:n_own].astype(bool)
     # send side (host, O(halo)): own positions of the rows this rank ships, per receiver
     pos = np.empty(n, dtype=np.int64)
@@ -126,9 +154,12 @@ def _op_layout(dcsr: _DevCsr, plan: CommPlan, kptr: int, bounds: np.ndarray, m: 
     if segs:
         np.cumsum([len(s) for s in segs], out=send_ptr[1:])
     send_idx = np.concatenate(segs) if segs else np.zeros(0, dtype=np.int64)
-    return OpLayout(n_own, n_halo, row_ptr.cpu().numpy(), ext.cpu().numpy()[:nnz].astype(np.int64),
-                    val.cpu().numpy()[:nnz], np.flatnonzero(~hh), np.flatnonzero(hh), recv, halo_off, halo_len,
-                    send_dst, send_ptr, send_idx, dst_slot)
+    tt = _tick("layout: host send side", tt)
+    out = OpLayout(n_own, n_halo, row_ptr.cpu().numpy(), ext.cpu().numpy()[:nnz].astype(np.int64),
+                   val.cpu().numpy()[:nnz], np.flatnonzero(~hh), np.flatnonzero(hh), recv, halo_off, halo_len,
+                   send_dst, send_ptr, send_idx, dst_slot)
+    _tick(f"layout: D2H + OpLayout ({nnz})", tt)
+    return out
 
 
 def build_layouts_device(a_fwd, a_bwd, pi, p: int | None, ranks, row_labels=None, device=None):
@@ -138,8 +169,12 @@ def build_layouts_device(a_fwd, a_bwd, pi, p: int | None, ranks, row_labels=None
     owner, p = _owner_and_p(pi, p)
     dev = device or torch.device("cuda", torch.cuda.current_device())
     out = {}
+    import time
+
     with torch.cuda.device(dev):
+        tt = _tick("upload fwd operator", time.perf_counter())
         df = _DevCsr(a_fwd, dev)
+        _tick("upload fwd operator", tt)
         plan_f, kf, bf, _, rank_ptr, _ = _plan(df, owner, p, dev)
         same = a_bwd is a_fwd
         if not same:
@@ -152,7 +187,7 @@ def build_layouts_device(a_fwd, a_bwd, pi, p: int | None, ranks, row_labels=None
                 rows = plan_f.rows_of(m)
                 if row_labels is not None:
                     rows = rows[np.lexsort((rows, np.asarray(row_labels)[rows]))]
-                    rows = degree_windows(rows, np.diff(np.asarray(a_fwd.row_offsets))[rows])
+                    rows = degree_windows(rows, np.diff(df.rp_host)[rows])
                 fwd = _op_layout(df, plan_f, kf, bf, m, rows, dev)
                 bwd = fwd if same else _op_layout(db, plan_b, kb, bb, m, rows, dev)
                 out[m] = RankLayout(m, p, rows, fwd, bwd)

@@ -134,10 +134,15 @@ def build_rank(a_hat, owner, p: int, rank: int, directed: bool, row_labels=None,
     on the GPU for large operators (devplan.py; identical to the host builders)."""
     from .runtime import _use_device_builder
 
-    if device is not None and _use_device_builder(a_hat, None):
+    from .devingest import DeviceGraph, transpose_device
+
+    if isinstance(a_hat, DeviceGraph) or (device is not None and _use_device_builder(a_hat, None)):
         from .devplan import build_layouts_device
 
-        a_bwd = transpose_sparse(a_hat) if directed else a_hat
+        if isinstance(a_hat, DeviceGraph):  # resident operator (mini-batch): transpose stays on the device
+            a_bwd = transpose_device(a_hat, keep_device=True) if directed else a_hat
+        else:
+            a_bwd = transpose_sparse(a_hat) if directed else a_hat
         plan_fwd, plan_bwd, lays = build_layouts_device(a_hat, a_bwd, np.asarray(owner), p, [rank],
                                                         row_labels=row_labels, device=device)
         return plan_fwd, plan_bwd, lays[rank]
@@ -811,7 +816,7 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
         t0 = time.perf_counter()
         batch = np.sort(rng.choice(n, size=spec_batch, replace=False))
         t1 = time.perf_counter()
-        sub_hat = _batch_operator(raw, batch, device)
+        sub_hat = _batch_operator(raw, batch, device, keep_device=True)
         t2 = time.perf_counter()
         sub_labels = _local_labelset(labels, batch)
         if sub_labels is None:  # no labelled vertex: ΔW = 0, weights unchanged (runtime.py:620-625)

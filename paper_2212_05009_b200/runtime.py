@@ -1312,7 +1312,7 @@ def _batch_features(mode, batch: np.ndarray, dev):
     return np.asarray(mode.features)[batch]
 
 
-def _batch_operator(adjacency, batch: np.ndarray, dev):
+def _batch_operator(adjacency, batch: np.ndarray, dev, keep_device: bool = False):
     """Renormalised induced sub-adjacency of a sorted batch (runtime.py:601-602):
     on the GPU for large graphs (devingest: the adjacency stays resident across
     steps; bit-identical to the host path), numpy otherwise.  The batch draw
@@ -1326,7 +1326,8 @@ def _batch_operator(adjacency, batch: np.ndarray, dev):
             g = (adjacency, DeviceGraph(adjacency, dev))
             _DEVICE_GRAPHS.clear()
             _DEVICE_GRAPHS[key] = g
-        return normalize_adjacency_device(induced_pattern_device(g[1], batch), dev)
+        return normalize_adjacency_device(induced_pattern_device(g[1], batch, keep_device=keep_device), dev,
+                                          keep_device=keep_device)
     return normalize_adjacency(induced_pattern(adjacency, batch, add_diagonal=False), add_self_loops=True)
 
 
