@@ -583,22 +583,23 @@ def bench_main(args, build_workload, ClockSampler, measured_peaks, roofline_summ
             from .hp import partition_hypergraph
 
             # the reference's defaults: 8 FM passes x 3 BFS restarts (partition.py)
-            pi = partition_hypergraph(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes, restarts=args.restarts,
-                                      directed=wl["directed"])
+            pi = partition_hypergraph(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes,
+                                      restarts=args.restarts, directed=wl["directed"])
         elif args.partition == "hp-ml":
             from .hp import partition_hypergraph_ml
 
-            pi = partition_hypergraph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes, restarts=args.restarts, labels=labels,
-                                         directed=wl["directed"])
+            pi = partition_hypergraph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes,
+                                         restarts=args.restarts, labels=labels, directed=wl["directed"])
         elif args.partition == "gp":
             from .hp import partition_graph
 
-            pi = partition_graph(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes, restarts=args.restarts, directed=wl["directed"])
+            pi = partition_graph(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes, restarts=args.restarts,
+                                 directed=wl["directed"])
         elif args.partition == "gp-ml":
             from .hp import partition_graph_ml
 
-            pi = partition_graph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes, restarts=args.restarts, labels=labels,
-                                    directed=wl["directed"])
+            pi = partition_graph_ml(wl["a_hat"], world, seed=args.seed, fm_passes=args.fm_passes,
+                                    restarts=args.restarts, labels=labels, directed=wl["directed"])
         else:
             pi = random_partition(wl["a_hat"].row_nnz(), PartitionConfig(p=world, seed=args.seed, epsilon=0.01))
         if args.locality == "on":
