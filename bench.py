@@ -235,7 +235,7 @@ def cpu_epochs(wl, n_epochs: int = 2, nthreads: int = 0, sample_ids=None):
     from oracle import gcn_oracle as o
 
     o.build()
-    threads = nthreads or o.max_threads()
+    threads = nthreads or max(o.max_threads(), len(os.sched_getaffinity(0)))
     a = o.as_csr(wl["a_hat"])
     a_back = o.transpose(a) if wl["directed"] else a
     ws = [np.asarray(w) for w in wl["model"].weights]
@@ -284,7 +284,9 @@ def run_reference(args):
     from oracle import gcn_oracle as o
 
     o.build()
-    threads = o.max_threads()
+    # all host cores: torchrun sets OMP_NUM_THREADS=1 for its ranks, which would
+    # leave the reference single-threaded at N > 1
+    threads = max(o.max_threads(), len(os.sched_getaffinity(0)))
     a = wl["a_hat"]
     a_back = o.transpose(a) if wl["directed"] else a
     ws = [np.asarray(w) for w in wl["weights"]]
