@@ -912,7 +912,15 @@ def scatter(a_hat, h0, pi, model, directed: bool = False, p: int | None = None, 
         if h0.shape != (a_hat.n_rows, model.dims[0]):
             raise ValueError(f"h0 has shape {h0.shape}, expected ({a_hat.n_rows}, {model.dims[0]})")
     dev = devmem.device(device)
-    a_bwd = transpose_sparse(a_hat) if directed else a_hat
+    from .devingest import DeviceGraph, transpose_device
+
+    resident = isinstance(a_hat, DeviceGraph)  # a mini-batch operator still on the device
+    if resident and (locality or not _use_device_builder(a_hat, builder)):
+        a_hat, resident = a_hat.to_host(), False
+    if resident:
+        a_bwd = transpose_device(a_hat, keep_device=True) if directed else a_hat
+    else:
+        a_bwd = transpose_sparse(a_hat) if directed else a_hat
     labels = None
     if locality:
         from .locality import locality_keys
@@ -1344,7 +1352,7 @@ def _train_minibatch(states, net, labels, epochs: int, mode, dev, scheduler: str
         losses = []
         for step in range(mode.batches_per_epoch):
             batch = np.sort(rng.choice(mode.adjacency.n_rows, size=mode.spec.batch_size, replace=False))
-            sub_hat = _batch_operator(mode.adjacency, batch, dev)
+            sub_hat = _batch_operator(mode.adjacency, batch, dev, keep_device=True)
             st0 = states[0]
             model = GcnModel(st0.dims, tuple(st0.weights), st0.activation, st0.learning_rate)
             feats = _batch_features(mode, batch, dev)

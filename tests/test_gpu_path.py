@@ -327,3 +327,37 @@ def test_reuse_fwd_aggregate_against_oracle(directed, p):
     # EpochMetrics also reports the reference's own word count for the same epoch
     assert [m.reference_words for m in metrics] == list(words)
     assert all(m.total_bytes > 0 for m in metrics) or p == 1
+
+
+def test_minibatch_resident_operator_matches_host_path(monkeypatch):
+    """Mini-batch steps on a graph above DEVICE_BUILDER_MIN_NNZ keep each batch
+    operator (and its transpose) on the device end to end; the results equal the
+    host-resident path's bit for bit (same operator bits, same layouts)."""
+    from paper_2212_05009_b200 import runtime as rt
+    from paper_2212_05009_b200 import synth
+
+    raw_p = synth.papers(0, n=1 << 17)
+    n = raw_p.n_rows
+    raw = gb.CsrMatrix(n, n, raw_p.row_offsets, raw_p.col_indices, raw_p.values)
+    assert raw.nnz >= rt.DEVICE_BUILDER_MIN_NNZ
+    dims = (16, 12, 6)
+    h0 = np.random.default_rng(4).standard_normal((n, dims[0]))
+    ids, y = o.random_labels(n, dims[-1], n // 10, 4)
+    labels = gb.LabelSet(ids, y, dims[-1])
+    model = gb.init_model(dims, 4)
+    owner = np.arange(n) * 3 // n
+    a_hat = gb.normalize_adjacency(raw)
+    pi = gb.Partition.from_assignment(owner, a_hat.row_nnz(), 3, 1.0)
+    mode = gb.MiniBatch(spec=gb.MiniBatchSpec(n // 2), batches_per_epoch=2, seed=3, adjacency=raw, features=h0,
+                        owner=owner, directed=True)
+    out = {}
+    for resident in (True, False):
+        if not resident:  # the round-2 path: the batch operator comes back to the host
+            orig = rt._batch_operator
+            monkeypatch.setattr(rt, "_batch_operator", lambda a, b, d, keep_device=False: orig(a, b, d, False))
+        states = gb.scatter(a_hat, h0, pi, model, directed=True)
+        m = gb.train_epochs(states, gb.DeviceNetwork(3), labels, 2, mode)
+        out[resident] = ([x.loss for x in m], [np.array(w) for w in states[0].weights], [x.total_words for x in m])
+    assert out[True][0] == out[False][0] and out[True][2] == out[False][2]
+    for a, b in zip(out[True][1], out[False][1]):
+        assert np.array_equal(a, b)
