@@ -805,17 +805,26 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
     from .host import GcnModel
     from .runtime import DeviceRows, _batch_operator, _local_labelset
 
+    from concurrent.futures import ThreadPoolExecutor
+
     rng = np.random.default_rng([int(seed), 0x7B])
     n = raw.n_rows
     losses, walls, words = [], [], []
     phases = {"draw": 0.0, "operator": 0.0, "setup": 0.0, "step": 0.0, "teardown": 0.0}
     ws = [np.asarray(w) for w in model.weights]
     cache: dict = {}
+    # the batch draws are the reference's sequential Generator stream and depend
+    # on nothing else: a one-worker thread draws step s+1's batch (same order,
+    # same values) while step s is set up and run
+    draws = ThreadPoolExecutor(max_workers=1)
+    draw = lambda: np.sort(rng.choice(n, size=spec_batch, replace=False))  # noqa: E731
+    pending = draws.submit(draw) if steps > 0 else None
     for step in range(steps):
         torch.cuda.synchronize(device)
         dist.barrier()
         t0 = time.perf_counter()
-        batch = np.sort(rng.choice(n, size=spec_batch, replace=False))
+        batch = pending.result()
+        pending = draws.submit(draw) if step + 1 < steps else None
         t1 = time.perf_counter()
         sub_hat = _batch_operator(raw, batch, device, keep_device=True)
         t2 = time.perf_counter()
@@ -860,6 +869,7 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
             for k, v in (("draw", t1 - t0), ("operator", t2 - t1), ("setup", t3 - t2), ("step", t4 - t3),
                          ("teardown", t5 - t4)):
                 phases[k] += v / max(steps - 1, 1)
+    draws.shutdown()
     dist.barrier()
     if cache.get("arena") is not None:
         DistributedTrainer._release_cached(cache)
