@@ -245,7 +245,7 @@ class DistributedTrainer:
 
     def __init__(self, a_hat, h0, owner, p: int, model, labels, directed: bool, device, timeout_ms: int = 20000,
                  row_labels=None, overlap: bool | None = None, reuse_fwd_aggregate: bool = False,
-                 arena_cache: dict | None = None):
+                 arena_cache: dict | None = None, labelled_restriction: bool = True):
         """row_labels: optional per-vertex community labels for the locality
         layout of own rows (locality.py); None keeps ascending global ids.
         overlap: split each layer into interior rows (computed while the halo
@@ -301,7 +301,7 @@ class DistributedTrainer:
         self.sched.skip_bwd1 = self.st.skips_bwd_exchange(1)
         assert self.st.transform_first == tf and self.st.n_pack == n_pack
         self.n_lab = len(labels)
-        self.st.set_labels(labels)
+        self.st.set_labels(labels, restrict=labelled_restriction)
         a = self.arena
         self.flags_halo = a.tensor("flags_halo", (p,), torch.int64)
         self.flags_ar = a.tensor("flags_ar", (p,), torch.int64)
@@ -357,9 +357,10 @@ class DistributedTrainer:
         # that is one launch over all own rows packs its rows (FusedPack)
         self.fuse_level = int(os.environ.get("GCNB_FUSE_PACK", "1"))
         self.fuse_pack = self.fuse_level > 0
-        if self.fuse_pack:
-            self.st.send_map("fwd")  # device arrays built now, never inside a graph capture
+        if self.fuse_pack:  # device arrays built now, never inside a graph capture
             self.st.send_map("bwd")
+            if self.fuse_level >= 2:
+                self.st.send_map("fwd")
         torch.cuda.synchronize(device)
         dist.barrier()
         self.graphs = {}
@@ -842,7 +843,8 @@ def train_minibatch(raw, features, owner, p: int, model, labels, spec_batch: int
             prof = cProfile.Profile()
             prof.enable()
         tr = DistributedTrainer(sub_hat, DeviceRows(features.feat, features.d, batch), np.asarray(owner)[batch], p, m,
-                                sub_labels, directed, device, timeout_ms=timeout_ms, overlap=False, arena_cache=cache)
+                                sub_labels, directed, device, timeout_ms=timeout_ms, overlap=False, arena_cache=cache,
+                                labelled_restriction=False)
         if prof is not None:
             import io
             import pstats

@@ -510,9 +510,12 @@ class ProcState:
     def stream(self):
         return torch.cuda.current_stream(self.device).cuda_stream
 
-    def set_labels(self, labels) -> int:
+    def set_labels(self, labels, restrict: bool = True) -> int:
         """Upload this rank's label map; returns its labelled-row count.  The
-        upload is skipped when the same (immutable) LabelSet is already resident."""
+        upload is skipped when the same (immutable) LabelSet is already resident.
+        restrict=False skips building the labelled-column operator of the last
+        layer's backward (§4.4 of DESIGN.md; exact either way): a mini-batch
+        operator serves one step, for which building it costs more than it saves."""
         if getattr(self, "_labels_obj", None) is labels:
             return self.n_labeled
         ids = np.asarray(labels.labeled_ids, dtype=np.int64)
@@ -533,7 +536,7 @@ class ProcState:
         self.label.copy_(torch.from_numpy(lab_map))
         self.n_labeled = count
         self._labels_obj = labels
-        self.op_bwd_lab = self._labelled_operator(lab_map, ids)
+        self.op_bwd_lab = self._labelled_operator(lab_map, ids) if restrict else None
         return count
 
     def _labelled_operator(self, lab_map: np.ndarray, labelled_ids: np.ndarray):
@@ -1250,7 +1253,7 @@ def parallel_backprop(states, net, labels, scheduler: str = "round", epoch: int 
 def _run_step(states, net, labels, n_lab: int, epoch: int, step: int, loss_slot: torch.Tensor,
               scheduler: str = "round") -> None:
     for st in states:
-        st.set_labels(labels)
+        st.set_labels(labels, restrict=False)  # one step per operator (mini-batch)
     rs = _streams_for(states, scheduler)
     _forward(states, net, epoch, step, rs)
     _backward(states, net, n_lab, epoch, step, loss_slot, rs)
