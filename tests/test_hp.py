@@ -194,3 +194,13 @@ def test_kway_refine_never_increases_cost_and_keeps_balance():
     assert pi1.is_balanced()
     again, _, _ = hp.kway_refine(a_hat, pi0.assignment, 4, w, 0.5)
     assert np.array_equal(owner, again)
+
+
+def test_multilevel_partition_parallel_levels_deterministic():
+    """partition_hypergraph_ml (per-level parallel bisection, concurrent restarts,
+    k-way refinement): balanced, and identical across runs despite the threads."""
+    raw = o.random_undirected(3000, 0.003, 9)
+    a_hat = gb.normalize_adjacency(gb.CsrMatrix(3000, 3000, raw.row_offsets, raw.col_indices, raw.values))
+    runs = [hp.partition_hypergraph_ml(a_hat, 4, seed=2, fm_passes=8, restarts=3, directed=False) for _ in range(3)]
+    assert all(r.is_balanced() for r in runs)
+    assert all(np.array_equal(runs[0].assignment, r.assignment) for r in runs[1:])
