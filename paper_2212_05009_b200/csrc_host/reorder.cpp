@@ -8,8 +8,11 @@
 // next to each other in the feature block — the gathers hit L2 instead of HBM.
 // This is a layout choice only: global vertex ids, plans and results are
 // unchanged.
+#include <omp.h>
+
 #include <algorithm>
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 extern "C" int gcnb_label_propagation(int64_t n, const int64_t* rp, const int64_t* ci, int32_t sweeps,
@@ -91,5 +94,116 @@ extern "C" int gcnb_chain_order(int64_t C, const int64_t* ptr, const int64_t* ad
       }
     }
   }
+  return 0;
+}
+
+// The contracted community graph chain_keys orders (locality.py): for labels
+// lab[0..n) in 0..C-1 and the pattern (rp, ci), the edge weight between
+// communities a != b is the number of nonzeros (u, v) with {lab[u], lab[v]} =
+// {a, b} counted in both directions (a nonzero u->v adds 1 to (a, b) and 1 to
+// (b, a)); edges sorted by (src, dst).  O(nnz + C + E log E) instead of numpy's
+// unique over 2·nnz keys.  Call with ptr/adj/w == nullptr for the edge count
+// (*m_out), then with arrays of C+1 / m / m entries.
+extern "C" int gcnb_community_graph(int64_t n, const int64_t* rp, const int64_t* ci, const int64_t* lab, int64_t C,
+                                    int64_t* m_out, int64_t* ptr, int64_t* adj, double* w) {
+  if (n < 0 || C < 0 || !rp || !ci || !lab || !m_out) return 1;
+  // members of each community (counting sort by label)
+  std::vector<int64_t> mptr(C + 1, 0), members(n);
+  for (int64_t v = 0; v < n; ++v) {
+    if (lab[v] < 0 || lab[v] >= C) return 1;
+    ++mptr[lab[v] + 1];
+  }
+  for (int64_t c = 0; c < C; ++c) mptr[c + 1] += mptr[c];
+  {
+    std::vector<int64_t> next(mptr.begin(), mptr.end() - 1);
+    for (int64_t v = 0; v < n; ++v) members[next[lab[v]]++] = v;
+  }
+  // out(a -> b): nonzeros from a's rows to b's columns, per a (dense counter +
+  // touched list per thread; communities in parallel, every host core)
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> outs(C);
+  int bad = 0;
+  const int nt = std::max(1, std::min(omp_get_num_procs(), 32));
+#pragma omp parallel num_threads(nt)
+  {
+    std::vector<int64_t> cnt(C, 0), touched;
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t a = 0; a < C; ++a) {
+      touched.clear();
+      for (int64_t i = mptr[a]; i < mptr[a + 1]; ++i) {
+        const int64_t u = members[i];
+        for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+          const int64_t v = ci[e];
+          if (v < 0 || v >= n) {
+            bad = 1;
+            continue;
+          }
+          const int64_t b = lab[v];
+          if (b == a) continue;
+          if (cnt[b]++ == 0) touched.push_back(b);
+        }
+      }
+      std::sort(touched.begin(), touched.end());
+      auto& o = outs[a];
+      o.reserve(touched.size());
+      for (int64_t b : touched) {
+        o.emplace_back(b, cnt[b]);
+        cnt[b] = 0;
+      }
+    }
+  }
+  if (bad) return 1;
+  std::vector<int64_t> optr(C + 1, 0);
+  for (int64_t a = 0; a < C; ++a) optr[a + 1] = optr[a] + (int64_t)outs[a].size();
+  std::vector<int64_t> odst(optr[C]), ocnt(optr[C]);
+  for (int64_t a = 0; a < C; ++a) {
+    int64_t k = optr[a];
+    for (const auto& pr : outs[a]) {
+      odst[k] = pr.first;
+      ocnt[k++] = pr.second;
+    }
+    std::vector<std::pair<int64_t, int64_t>>().swap(outs[a]);
+  }
+  // symmetric weights: w(a, b) = out(a -> b) + out(b -> a); the reverse lists by a counting sort
+  const int64_t E = (int64_t)odst.size();
+  std::vector<int64_t> rptr(C + 1, 0), rsrc(E), rcnt(E);
+  for (int64_t e = 0; e < E; ++e) ++rptr[odst[e] + 1];
+  for (int64_t c = 0; c < C; ++c) rptr[c + 1] += rptr[c];
+  {
+    std::vector<int64_t> next(rptr.begin(), rptr.end() - 1);
+    for (int64_t a = 0; a < C; ++a)  // a ascending: each reverse list comes out sorted by source
+      for (int64_t e = optr[a]; e < optr[a + 1]; ++e) {
+        const int64_t k = next[odst[e]]++;
+        rsrc[k] = a;
+        rcnt[k] = ocnt[e];
+      }
+  }
+  // merge the two sorted lists of every community
+  int64_t m = 0;
+  const bool fill = ptr && adj && w;
+  if (fill) ptr[0] = 0;
+  for (int64_t a = 0; a < C; ++a) {
+    int64_t i = optr[a], j = rptr[a];
+    while (i < optr[a + 1] || j < rptr[a + 1]) {
+      int64_t b;
+      double x = 0.0;
+      if (j >= rptr[a + 1] || (i < optr[a + 1] && odst[i] < rsrc[j])) {
+        b = odst[i];
+        x = (double)ocnt[i++];
+      } else if (i >= optr[a + 1] || rsrc[j] < odst[i]) {
+        b = rsrc[j];
+        x = (double)rcnt[j++];
+      } else {
+        b = odst[i];
+        x = (double)(ocnt[i++] + rcnt[j++]);
+      }
+      if (fill) {
+        adj[m] = b;
+        w[m] = x;
+      }
+      ++m;
+    }
+    if (fill) ptr[a + 1] = m;
+  }
+  *m_out = m;
   return 0;
 }

@@ -64,6 +64,8 @@ def _load():
         lib.gcnb_csr_transpose.restype = ctypes.c_int
         lib.gcnb_searchsorted_f64.argtypes = [vp, i64, vp, i64, vp]
         lib.gcnb_coarse_column_nets.argtypes = [i64, vp, vp, vp, i64, vp, vp, vp, vp]
+        lib.gcnb_community_graph.argtypes = [i64, vp, vp, vp, i64, vp, vp, vp, vp]
+        lib.gcnb_community_graph.restype = ctypes.c_int
         lib.gcnb_kway_refine.argtypes = [i64, vp, vp, vp, ctypes.c_int32, vp, f64, ctypes.c_int32, vp, vp]
         lib.gcnb_kway_refine.restype = ctypes.c_int
         lib.gcnb_coarse_column_nets.restype = ctypes.c_int

@@ -44,9 +44,44 @@ def chain_keys(a, labels: np.ndarray) -> np.ndarray:
     (gcnb_chain_order over the community graph, edge weight = number of Â
     nonzeros between two communities, starting from the largest community)."""
     _, lab = np.unique(np.asarray(labels), return_inverse=True)
+    lab = np.ascontiguousarray(lab, dtype=np.int64)
     C = int(lab.max()) + 1 if len(lab) else 0
-    ro = np.asarray(a.row_offsets, dtype=np.int64)
-    ci = np.asarray(a.col_indices, dtype=np.int64)
+    ro = np.ascontiguousarray(a.row_offsets, dtype=np.int64)
+    ci = np.ascontiguousarray(a.col_indices, dtype=np.int64)
+    ptr, adj, w = community_graph(a.n_rows, ro, ci, lab, C)
+    rank = np.empty(C, dtype=np.int64)
+    start = int(np.argmax(np.bincount(lab, minlength=C))) if C else 0
+    rc = hp._load().gcnb_chain_order(C, ptr.ctypes.data, adj.ctypes.data, w.ctypes.data, start, rank.ctypes.data)
+    if rc != 0:
+        raise ValueError("chain order: invalid community graph")
+    return rank[lab]
+
+
+# numpy's hashed unique wins below this many nonzeros (amazon0601, roadNet); the
+# parallel native pass above it (products: 6.9 -> 1.7 s on 8 cores)
+NATIVE_GRAPH_MIN_NNZ = 1 << 25
+
+
+def community_graph(n: int, ro: np.ndarray, ci: np.ndarray, lab: np.ndarray, C: int):
+    """(ptr, adj, w) of the contracted community graph: w(a, b) = nonzeros between
+    communities a != b counted both ways, edges sorted by (src, dst); in O(nnz)
+    (csrc_host/reorder.cpp gcnb_community_graph), numpy restatement below."""
+    try:
+        lib = hp._load() if len(ci) >= NATIVE_GRAPH_MIN_NNZ else None
+    except ImportError:
+        lib = None
+    if lib is not None:
+        import ctypes
+
+        m = ctypes.c_int64(0)
+        args = (n, ro.ctypes.data, ci.ctypes.data, lab.ctypes.data, C, ctypes.byref(m))
+        if lib.gcnb_community_graph(*args, None, None, None) != 0:
+            raise ValueError("community graph: invalid input")
+        ptr = np.zeros(C + 1, dtype=np.int64)
+        adj = np.empty(max(m.value, 1), dtype=np.int64)
+        w = np.empty(max(m.value, 1), dtype=np.float64)
+        lib.gcnb_community_graph(*args, ptr.ctypes.data, adj.ctypes.data, w.ctypes.data)
+        return ptr, adj[: m.value], w[: m.value]
     cu = np.repeat(lab, np.diff(ro))
     cv = lab[ci]
     off = cu != cv
@@ -54,14 +89,7 @@ def chain_keys(a, labels: np.ndarray) -> np.ndarray:
     src, dst = key // C, key % C
     ptr = np.zeros(C + 1, dtype=np.int64)
     np.cumsum(np.bincount(src, minlength=C), out=ptr[1:])
-    adj = np.ascontiguousarray(dst, dtype=np.int64)
-    w = np.ascontiguousarray(cnt, dtype=np.float64)
-    rank = np.empty(C, dtype=np.int64)
-    start = int(np.argmax(np.bincount(lab, minlength=C))) if C else 0
-    rc = hp._load().gcnb_chain_order(C, ptr.ctypes.data, adj.ctypes.data, w.ctypes.data, start, rank.ctypes.data)
-    if rc != 0:
-        raise ValueError("chain order: invalid community graph")
-    return rank[lab]
+    return ptr, np.ascontiguousarray(dst, dtype=np.int64), np.ascontiguousarray(cnt, dtype=np.float64)
 
 
 def locality_keys(a, sweeps: int = 5, symmetric: bool | None = None) -> np.ndarray:

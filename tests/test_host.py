@@ -273,3 +273,29 @@ def test_compat_install_rebinds_reference_names():
     finally:
         compat.uninstall(gcnpart)
     assert gcnpart.scatter is orig
+
+
+def test_community_graph_native_matches_numpy(monkeypatch):
+    """gcnb_community_graph (csrc_host/reorder.cpp) equals the numpy restatement."""
+    import numpy as np
+
+    from paper_2212_05009_b200 import hp, locality
+    from oracle import gcn_oracle as o
+
+    raw = o.random_directed(1500, 0.01, 3)
+    ro = np.ascontiguousarray(raw.row_offsets, dtype=np.int64)
+    ci = np.ascontiguousarray(raw.col_indices, dtype=np.int64)
+    lab = np.ascontiguousarray(np.random.default_rng(1).integers(0, 40, 1500), dtype=np.int64)
+    _, lab = np.unique(lab, return_inverse=True)
+    lab = np.ascontiguousarray(lab, dtype=np.int64)
+    C = int(lab.max()) + 1
+    monkeypatch.setattr(locality, "NATIVE_GRAPH_MIN_NNZ", 0)
+    native = locality.community_graph(1500, ro, ci, lab, C)
+
+    def no_lib():
+        raise ImportError("forced")
+
+    monkeypatch.setattr(hp, "_load", no_lib)
+    ref = locality.community_graph(1500, ro, ci, lab, C)
+    for x, y in zip(native, ref):
+        assert np.array_equal(x, y)
